@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark of the depth-first stack executor on BASELINE.json's metric.
+
+metric : "fused-stack HBM GB/s (% of B200 peak) and images/sec at 1/2/4/8 GPUs"
+value  : whole-job images/s (all ranks) for one pass of every stack of the workload over
+         one batch per rank ("step"); GB/s and % of the measured HBM peak ride alongside.
+default workload: configs[1], AlexNet's three ReLU->MaxPool3x3/s2 stacks at batch 128
+         (`--workload vgg16|resnet50|densenet121|c1` selects the other configs).
+
+Multi-GPU (torchrun, one process per GPU): every rank runs its own batch (weak scaling,
+the batch dimension is the unit that shards); no collective on the data path.  NCCL is
+used only after the timed region: max-over-ranks time and per-rank output checksums.
+
+Timing: W warm-up steps, then K steps between barrier + cuda.synchronize on both sides,
+CUDA events on the launching stream; inputs rotate over enough buffer sets to exceed
+4x the L2 (or are larger than L2).  The dominant kernel is timed with events around its
+own launches for the roofline object.  `--impl reference` times the CPU oracle instead
+(rank 0 only), a bounded sample of images per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "fused-stack HBM GB/s (% of B200 peak) and images/sec at 1/2/4/8 GPUs"
+CONFIG_INDEX = {"c1": 0, "alexnet": 1, "vgg16": 2, "resnet50": 3, "densenet121": 4}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json, b.copy_(a) read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def instances(cases):
+    out = []
+    for c in cases:
+        out += [c] * c.count
+    return out
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed region runs."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: report what we have
+            self.nv = None
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.002)
+
+    def sample(self):
+        if self.nv is None:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def __enter__(self):
+        self.sample()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join()
+        self.sample()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle timing
+def time_oracle(cases, budget_s: float, max_images: int):
+    """The oracle as it stands (single thread) on whole images of the workload."""
+    import oracle
+    oracle.build()
+    def one_image(k):
+        for c in cases:
+            shp = (1,) + tuple(c.shape[1:])
+            x = synth.uniform_np(c.input_seed, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
+            for _ in range(c.count):
+                oracle.run_bf(c.layers, x)
+    t0 = time.perf_counter()
+    one_image(0)
+    t1 = time.perf_counter() - t0
+    n = int(max(1, min(max_images, budget_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    for k in range(n):
+        one_image(k)
+    T = time.perf_counter() - t0
+    return n / T, n, T
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cases = synth.workload(args.workload, batch=1)
+    import oracle
+    oracle.build()
+    def step(k):
+        for c in cases:
+            shp = (1,) + tuple(c.shape[1:])
+            x = synth.uniform_np(c.input_seed, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
+            for _ in range(c.count):
+                oracle.run_bf(c.layers, x)
+    for k in range(args.warmup):
+        step(k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        step(args.warmup + k)
+    T = time.perf_counter() - t0
+    ips = args.steps / T
+    batch = synth.DEFAULT_BATCH[args.workload]
+    line = {"impl": "reference", "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 arithmetic, f32 tensors",
+            "data": "synthetic (SplitMix64, seeded)",
+            "config": {"workload": args.workload, "baseline_config_index": CONFIG_INDEX[args.workload],
+                       "global_batch": batch, "parallelism": "none (host CPU oracle)"},
+            "cpu_baseline": {"value": ips, "unit": "images/s", "cores": 1, "kind": "oracle",
+                             "sample": f"1 image of the batch-{batch} {args.workload} workload per step "
+                                       f"(every stack), breadth-first C oracle, single thread"},
+            "e2e": {"value": ips, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU bench
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="brainslug", choices=["brainslug", "reference"])
+    ap.add_argument("--workload", default="alexnet", choices=list(CONFIG_INDEX))
+    ap.add_argument("--batch", type=int, default=0, help="per-rank batch (0 = BASELINE.json batch)")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lbl", action="store_true", help="skip the torch layer-by-layer context number")
+    ap.add_argument("--out", default="", help="also append the JSON line to this file")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_08378_b200 as bs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    batch = args.batch or synth.DEFAULT_BATCH[args.workload]
+    cases = synth.workload(args.workload, batch=batch)
+    inst = instances(cases)
+    plans = {}
+    for c in cases:
+        plans[c.name] = bs.bs_plan_create(c.layers, c.shape)
+    infos = {c.name: bs.bs_plan_query(plans[c.name]) for c in cases}
+    launches_per_step = sum(infos[c.name]["n_launches"] for c in inst)
+    step_bytes = sum(infos[c.name]["alg_bytes_read"] + infos[c.name]["alg_bytes_written"] for c in inst)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    n_sets = 1 if step_bytes >= 8 * l2 else int(math.ceil(4 * l2 / step_bytes)) + 1
+    # buffers: per instance per set (inputs distinct per instance so nothing is re-read from L2)
+    bufs = []
+    for s in range(n_sets):
+        row = []
+        for j, c in enumerate(inst):
+            x = synth.uniform_torch(c.input_seed + 7 * j, c.shape, device=dev, start=rank * int(np.prod(c.shape)))
+            y = torch.empty(infos[c.name]["out"], device=dev)
+            row.append((x, y))
+        bufs.append(row)
+    # dominant instance: the most algorithmic bytes
+    dom = max(range(len(inst)), key=lambda j: infos[inst[j].name]["alg_bytes_read"] + infos[inst[j].name]["alg_bytes_written"])
+    dom_info = bs.bs_plan_query_launch(plans[inst[dom].name], 0)
+    dom_bytes = infos[inst[dom].name]["alg_bytes_read"] + infos[inst[dom].name]["alg_bytes_written"]
+
+    stream = torch.cuda.Stream(device=dev)
+    sh = stream.cuda_stream
+    handles = [plans[c.name] for c in inst]
+
+    def step(k, ev=None):
+        row = bufs[k % n_sets]
+        for j, h in enumerate(handles):
+            x, y = row[j]
+            if ev is not None and j == dom:
+                ev[0].record(stream)
+                bs.bs_execute(h, x.data_ptr(), y.data_ptr(), sh)
+                ev[1].record(stream)
+            else:
+                bs.bs_execute(h, x.data_ptr(), y.data_ptr(), sh)
+
+    with torch.cuda.stream(stream):
+        for k in range(args.warmup):
+            step(k)
+    torch.cuda.synchronize()
+    dom_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k, dom_events[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    dom_ms = float(np.mean([a.elapsed_time(b) for a, b in dom_events]))
+    # checksum of the last step's outputs (fp64 sum) -- gathered below, outside the timing
+    last = bufs[(args.warmup + args.steps - 1) % n_sets]
+    csum = float(sum(y.double().sum().item() for _, y in last))
+    finite = all(bool(torch.isfinite(y).all()) for _, y in last)
+    if world > 1:
+        t = torch.tensor([ms, dom_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, dom_ms = float(t[0]), float(t[1])
+        cs = torch.tensor([csum, float(finite)], device=dev, dtype=torch.float64)
+        gathered = [torch.zeros_like(cs) for _ in range(world)]
+        dist.all_gather(gathered, cs)
+        checksums = [float(g[0]) for g in gathered]
+        finite = all(bool(g[1]) for g in gathered)
+    else:
+        checksums = [csum]
+
+    ms_step = ms / args.steps
+    images = batch * world
+    ips = images / (ms_step / 1e3)
+    gbs_rank = step_bytes / (ms_step / 1e3) / 1e9
+    peak, peak_src = load_peaks()
+    dom_achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+
+    # ---- end to end: host buffers through bs_execute_host (H2D + kernels + D2H every step)
+    e2e = None
+    e2e_steps = args.e2e_steps or max(3, min(20, args.steps // 10))
+    max_in = max(infos[c.name]["alg_bytes_read"] for c in cases) // 4
+    max_out = max(infos[c.name]["alg_bytes_written"] for c in cases) // 4
+    h_in = torch.empty(max_in, dtype=torch.float32).pin_memory()
+    h_in.copy_(synth.uniform_torch(99, (max_in,), device=dev).cpu())
+    h_out = torch.empty(max_out, dtype=torch.float32).pin_memory()
+    h2d = sum(infos[c.name]["alg_bytes_read"] for c in inst)
+    d2h = sum(infos[c.name]["alg_bytes_written"] for c in inst)
+
+    def e2e_step(k):
+        row = bufs[k % n_sets]
+        for j, h in enumerate(handles):
+            x, y = row[j]
+            bs.bs_execute_host(h, [h_in.data_ptr()], h_out.data_ptr(), [x.data_ptr()], y.data_ptr(), 0, sh)
+
+    e2e_step(0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for k in range(e2e_steps):
+        e2e_step(k)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    e2e = {"value": images / (e2e_ms / e2e_steps / 1e3), "unit": "images/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+           "path": "bs_execute_host: pinned host -> device copy, kernels, device -> host copy, pipelined per chunk"}
+
+    # ---- layer-by-layer torch eager on the same GPU (the paper's comparison system, re-hosted)
+    lbl = None
+    if not args.no_lbl and rank == 0:
+        import torch.nn.functional as F
+        params = {}
+        for c in cases:
+            ps = []
+            for L in c.layers:
+                if L.kind == "batchnorm":
+                    ps.append(tuple(torch.from_numpy(getattr(L, f)).to(dev) for f in ("mean", "var", "gamma", "beta")))
+                else:
+                    ps.append(None)
+            params[c.name] = ps
+
+        def lbl_step(k):
+            row = bufs[k % n_sets]
+            for j, c in enumerate(inst):
+                t = row[j][0]
+                for L, p in zip(c.layers, params[c.name]):
+                    if L.kind == "batchnorm":
+                        t = F.batch_norm(t, p[0], p[1], p[2], p[3], False, 0.0, L.eps)
+                    elif L.kind == "relu":
+                        t = F.relu(t)
+                    elif L.kind == "maxpool":
+                        t = F.max_pool2d(t, L.kernel, L.stride, L.padding)
+                    elif L.kind == "avgpool":
+                        t = F.avg_pool2d(t, L.kernel, L.stride, L.padding, count_include_pad=L.count_include_pad)
+        lsteps = max(3, min(50, args.steps // 4))
+        with torch.cuda.stream(stream):
+            for k in range(3):
+                lbl_step(k)
+            torch.cuda.synchronize()
+            a.record(stream)
+            for k in range(lsteps):
+                lbl_step(k)
+            b.record(stream)
+        torch.cuda.synchronize()
+        lbl_ms = a.elapsed_time(b) / lsteps
+        lbl = {"images_per_s": batch / (lbl_ms / 1e3), "ms_per_step": lbl_ms,
+               "fused_speedup": lbl_ms / ms_step,
+               "what": "torch eager F.batch_norm/relu/max_pool2d/avg_pool2d, one kernel per layer, same GPU"}
+
+    # ---- CPU oracle baseline on a bounded sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, n, T = time_oracle(cases, args.cpu_budget, batch)
+        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle",
+               "sample": f"{n} images of the batch-{batch} {args.workload} workload (all stacks), "
+                         f"breadth-first C oracle, single thread, {T:.1f} s"}
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        tr = json.load(open(tp))
+        key = f"{args.workload}:{inst[dom].name}"
+        if key in tr:
+            traffic = tr[key]["dram_bytes_per_launch"]
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 seeded NCHW fp32, BN params per SURVEY §8(d))",
+            "config": {"workload": args.workload, "baseline_config_index": CONFIG_INDEX[args.workload],
+                       "global_batch": images, "per_gpu_batch": batch, "stacks_per_step": len(inst),
+                       "parallelism": f"batch-sharded dp{world} (independent images, no data-path collective)",
+                       "l2": (f"rotating {n_sets} buffer sets ({n_sets * step_bytes / 1e9:.2f} GB > 4x L2 "
+                              f"{l2 / 1e6:.0f} MB)") if n_sets > 1 else
+                             f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB per step vs {l2 / 1e6:.0f} MB)"},
+            "hbm": {"alg_gbs_per_gpu": gbs_rank, "alg_gbs_total": gbs_rank * world,
+                    "pct_of_measured_peak": 100 * gbs_rank / peak, "pct_of_8tbs": 100 * gbs_rank / 8000.0,
+                    "alg_bytes_per_step_per_gpu": step_bytes},
+            "roofline": {"bound": "hbm", "achieved": dom_achieved, "peak": peak, "unit": "GB/s",
+                         "frac": dom_achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": bs.KERNEL_NAMES[dom_info["kernel"]], "stack": inst[dom].name,
+                         "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "layer_by_layer_torch": lbl,
+            "checksums": checksums, "outputs_finite": finite,
+        }
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            with open(args.out, "a") as f:
+                f.write(s + "\n")
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,210 @@
+/*
+ * bs.h -- C ABI of the B200-native BrainSlug stack executor.
+ *
+ * BrainSlug (arXiv:1804.08378) accelerates a *stack* -- a maximal run of consecutive
+ * element-wise and pooling layers (§3.2 "Aggregation Detection") --
+ * by executing it depth-first: each tile of the input is read from main memory once,
+ * pushed through every layer of the stack on-chip, and written once (fig:trio-df,
+ * P:L208-239; §3.1), instead of one memory round-trip per layer.
+ *
+ * The interface follows the paper's two phases (fig:brainslug-arch P:L378-411):
+ *   compile phase  -> bs_plan_create: validate the layer list, map layers to
+ *                                   operations, group operations into steps and steps into
+ *                                   sequences, size tiles/halos for the device;
+ *   execution phase -> bs_execute: "calculates the output size ... loaded,
+ *                                   executed"; sequences run serialised.
+ * Kernels are hand-written, ahead-of-time compiled for sm_100a (no code generation).
+ *
+ * Conventions for every function:
+ *  - extern "C", no C++ types or exceptions cross the boundary; errors are return codes,
+ *    with a thread-local message from bs_last_error() naming the layer index and field.
+ *  - Tensors: contiguous NCHW fp32, exactly N*C*H*W elements, DEVICE pointers on the
+ *    plan's device unless a function says "host".  No strides/views.
+ *  - bs_execute* only ENQUEUE work on the caller's stream: no allocation, no host sync,
+ *    no host<->device copy (except bs_execute_host, whose job is exactly those copies).
+ *    Asynchronous device faults surface at the caller's next synchronisation.
+ *  - Plans are immutable after creation; concurrent bs_execute on different streams is
+ *    safe.  bs_plan_create is reentrant.
+ */
+#ifndef BS_H
+#define BS_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BS_API __attribute__((visibility("default")))
+#else
+#define BS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *bs_stream_t;   /* == cudaStream_t; NULL = legacy default stream */
+typedef struct bs_plan bs_plan;            /* opaque, immutable after create */
+
+typedef enum {
+    BS_OK = 0,
+    BS_ERR_INVALID_ARGUMENT = 2, /* NULL pointer, n_layers < 1, unknown kind, non-positive dim,
+                                    misaligned (not 16-B) or overlapping tensor pointers,
+                                    wrong number of inputs, execute on a host-only plan */
+    BS_ERR_VALIDATION = 3,       /* k < 1, s < 1, p < 0 or p > k/2, pool extent < 1,
+                                    eps <= 0, var < 0, NULL BN array, bad ADD operand index */
+    BS_ERR_PLANNING = 4,         /* CONV2D / LINEAR in the stack (opaque: not optimizable,
+                                    P:L135-146); tensor too large for the index
+                                    types */
+    BS_ERR_CUDA = 6,             /* CUDA error during create (alloc/copy/attributes) or launch */
+    BS_ERR_OUT_OF_MEMORY = 7     /* device allocation of plan-owned memory failed */
+} bs_status;
+
+typedef enum {
+    BS_OP_BATCHNORM = 1,  /* inference BN, folded to a per-channel affine (north_star)     */
+    BS_OP_RELU = 2,       /* f(x) = max(0, x); +0.0 for x <= 0               */
+    BS_OP_MAXPOOL = 3,    /* window max, padded cells absent                */
+    BS_OP_AVGPOOL = 4,    /* window sum + "AvgNormalization" (lst:finalcode P:L520-524)    */
+    BS_OP_COPY = 5,       /* identity (eval-mode Dropout); elided                        */
+    BS_OP_SCALE = 6,      /* y = alpha * x                                                */
+    BS_OP_ADD = 7,        /* y = x + operand (residual add)                               */
+    BS_OP_CONV2D = 100,   /* representable so a front-end can pass a whole chain; always  */
+    BS_OP_LINEAR = 101    /* rejected with BS_ERR_PLANNING                                 */
+} bs_op_kind;
+
+/* One layer.  Unused fields are ignored for other kinds. */
+typedef struct {
+    int32_t kind;                                   /* bs_op_kind */
+    int32_t kernel_h, kernel_w;                     /* pools: k >= 1 */
+    int32_t stride_h, stride_w;                     /* pools: s >= 1 */
+    int32_t pad_h, pad_w;                           /* pools: 0 <= p <= k/2 (PyTorch rule) */
+    int32_t count_include_pad;                      /* avgpool: 1 = divisor k_h*k_w (PyTorch default) */
+    float eps;                                      /* BN: > 0 */
+    const float *gamma, *beta, *running_mean, *running_var; /* BN: HOST arrays, length = C;
+                                                       copied during bs_plan_create */
+    float alpha;                                    /* SCALE */
+    int32_t operand;                                /* ADD: index >= 1 into bs_execute_ex inputs[] */
+} bs_layer_desc;
+
+typedef struct { int64_t n, c, h, w; } bs_shape;
+
+/* Options; pass NULL for the defaults of the current device. */
+typedef struct {
+    int32_t device;                 /* CUDA device ordinal; -1 = current device */
+    int32_t host_only;              /* 1 = plan on the host only (no device memory; the plan can
+                                       be queried but not executed); used by CPU tests */
+    int32_t max_steps_per_sequence; /* 0 = unlimited; 1 and 5 mirror the paper's policies
+                                       (P:L677-678).  This build executes one step per sequence
+                                       (see DESIGN.md), so values other than 1 are clamped. */
+    int32_t threads_per_block;      /* 0 = planner default (multiple of 32, <= 1024) */
+    int32_t force_rows_per_task;    /* 0 = planner; >0 forces the output-row band of a pool
+                                       tile (tests use it: results must not depend on tiling) */
+    int32_t force_outputs_per_group;/* 0 = planner; >0 forces output columns per lane group */
+    int32_t force_generic;          /* 1 = use the runtime-geometry pool kernel even where a
+                                       specialised one exists (tests) */
+    int32_t reserved[5];
+} bs_plan_options;
+
+/* Whole-plan summary. */
+typedef struct {
+    bs_shape out;                   /* output shape of the stack */
+    int32_t n_layers, n_ops;        /* ops = layers minus elided COPYs */
+    int32_t n_steps, n_sequences, n_launches;
+    int32_t n_inputs;               /* 1 + number of ADD operands */
+    int64_t alg_bytes_read;         /* one read of the input + every ADD operand */
+    int64_t alg_bytes_written;      /* one write of the output */
+    int64_t param_bytes;            /* folded per-channel parameters held on the device */
+    int64_t intermediate_bytes;     /* plan-owned buffers between serialised sequences */
+} bs_plan_info;
+
+/* Per-launch (= per sequence) details. */
+typedef struct {
+    int32_t kernel;                 /* 1 = element-wise streaming, 2 = pool column-walker
+                                       (specialised k/s), 3 = pool column-walker (runtime
+                                       geometry), 4 = pool one-thread-per-output */
+    int32_t first_layer, last_layer;/* layer index range [first, last] covered */
+    bs_shape in, out;
+    int32_t pool_kh, pool_kw, pool_sh, pool_sw, pool_ph, pool_pw;  /* 0 if no pool */
+    int32_t n_prologue_ops, n_epilogue_ops;
+    int32_t grid, block;
+    int32_t groups_per_warp;        /* lane groups (one plane each) packed in a warp */
+    int32_t outputs_per_group;      /* output columns produced by one lane group */
+    int32_t rows_per_task;          /* output rows walked by one warp task */
+    int32_t halo_rows;              /* input rows re-read between row bands (k - s, >= 0) */
+    int64_t n_tasks;                /* warp tasks */
+    int64_t alg_bytes_read, alg_bytes_written;
+} bs_launch_info;
+
+/*
+ * bs_plan_create -- compile phase.
+ *   layers/n_layers : the stack, in network order (host memory; copied).
+ *   input           : (N, C, H, W) of the stack input; all >= 1.
+ *   opts            : NULL = defaults on the current device.
+ *   plan_out        : receives the plan (NULL on failure).
+ * Steps performed: validation + shape inference (a1); layer -> op mapping with BN folded
+ * in fp64 to scale = gamma/sqrt(var+eps), shift = beta - mean*scale, rounded once to fp32
+ * (a2); greedy step grouping -- an element-wise op always joins the current step, a pool
+ * joins only if the step has none (prose rule) (a3); sequence
+ * packing and tile geometry for the device (a4).
+ * Allocates device memory for folded parameters (8*C bytes per BN) and for intermediates
+ * between serialised sequences; the plan owns it.
+ * Errors: BS_ERR_INVALID_ARGUMENT / VALIDATION / PLANNING / CUDA / OUT_OF_MEMORY.
+ */
+BS_API bs_status bs_plan_create(const bs_layer_desc *layers, int32_t n_layers, bs_shape input,
+                         const bs_plan_options *opts, bs_plan **plan_out);
+
+/* bs_plan_query -- fill *info.  Errors: BS_ERR_INVALID_ARGUMENT on NULL. */
+BS_API bs_status bs_plan_query(const bs_plan *plan, bs_plan_info *info);
+
+/* bs_plan_query_launch -- details of launch `index` in [0, n_launches). */
+BS_API bs_status bs_plan_query_launch(const bs_plan *plan, int32_t index, bs_launch_info *info);
+
+/*
+ * bs_execute -- execution phase for stacks without ADD.
+ *   in  : device pointer, input shape, 16-B aligned.
+ *   out : device pointer, bs_plan_info.out shape, 16-B aligned; must not overlap `in`,
+ *         except exactly in == out for plans whose every step is element-wise (in-place).
+ *   stream : CUDA stream the n_launches kernels are enqueued on, in order.
+ * Errors: BS_ERR_INVALID_ARGUMENT (NULL/misaligned/overlap/plan needs operands/host-only
+ * plan), BS_ERR_CUDA (launch failure; message in bs_last_error()).
+ */
+BS_API bs_status bs_execute(const bs_plan *plan, const float *in, float *out, bs_stream_t stream);
+
+/*
+ * bs_execute_ex -- as bs_execute with ADD operands.
+ *   inputs[0] = stack input; inputs[k] = operand k (shape = the ADD layer's input shape).
+ *   n_inputs must equal bs_plan_info.n_inputs.
+ */
+BS_API bs_status bs_execute_ex(const bs_plan *plan, const float *const *inputs, int32_t n_inputs,
+                        float *out, bs_stream_t stream);
+
+/*
+ * bs_execute_host -- end-to-end execution from HOST buffers.
+ *   h_inputs[n_inputs] : host pointers (pinned for copy/compute overlap; pageable works
+ *                        but serialises), same shapes as bs_execute_ex.
+ *   h_out              : host pointer for the output.
+ *   d_inputs[n_inputs], d_out : caller-owned device buffers of the same shapes (staging).
+ *   n_chunks           : the batch is split into n_chunks image ranges; chunk k's
+ *                        host->device copy, kernels, and device->host copy are pipelined
+ *                        across the plan's two copy streams and `stream` (0 = planner picks).
+ * Returns after ENQUEUEING; the caller synchronises `stream` before reading h_out.
+ */
+BS_API bs_status bs_execute_host(const bs_plan *plan, const float *const *h_inputs, int32_t n_inputs,
+                          float *h_out, float *const *d_inputs, float *d_out,
+                          int32_t n_chunks, bs_stream_t stream);
+
+/* bs_plan_destroy -- frees plan-owned device memory and streams.  NULL-safe.  The caller
+ * must ensure no execution using the plan is still in flight. */
+BS_API void bs_plan_destroy(bs_plan *plan);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+BS_API const char *bs_last_error(void);
+
+/* Static name of a status code. */
+BS_API const char *bs_status_string(bs_status s);
+
+/* Library version, for the binding's sanity check. */
+BS_API int32_t bs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BS_H */

@@ -1,0 +1,795 @@
+// bs_api.cpp -- the C ABI (include/bs.h): planner (compile phase) and
+// runtime (execution phase) of the B200 depth-first stack executor.
+//
+//   a1 validate + shape inference ........ validate_and_shape()
+//   a2 layer -> ops, BN folding ........... map_ops()
+//   a3 step grouping ...................... group_steps()
+//   a4 sequence packing + tile geometry ... pack_and_tile()
+//   a5 dispatch ........................... enqueue()
+//
+// See DESIGN.md for the B200 tile policy and how it differs from the paper's.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/bs.h"
+#include "bs_internal.h"
+
+using namespace bs;
+
+namespace {
+
+thread_local std::string g_err;
+
+bs_status fail(bs_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+const char* kind_name(int k) {
+  switch (k) {
+    case BS_OP_BATCHNORM: return "batchnorm";
+    case BS_OP_RELU: return "relu";
+    case BS_OP_MAXPOOL: return "maxpool";
+    case BS_OP_AVGPOOL: return "avgpool";
+    case BS_OP_COPY: return "copy";
+    case BS_OP_SCALE: return "scale";
+    case BS_OP_ADD: return "add";
+    case BS_OP_CONV2D: return "conv2d";
+    case BS_OP_LINEAR: return "linear";
+    default: return "?";
+  }
+}
+
+bool is_pool(int k) { return k == BS_OP_MAXPOOL || k == BS_OP_AVGPOOL; }
+
+struct Shape4 {
+  int64_t n, c, h, w;
+  int64_t numel() const { return n * c * h * w; }
+};
+
+// A host-side element-wise op.
+struct HostOp {
+  int32_t kind;                   // DevOp
+  int32_t layer;                  // source layer index
+  std::vector<float2> affine;     // DOP_AFFINE: folded (scale, shift) per channel
+  size_t affine_off = 0;          // offset (in float2) into the plan's parameter block
+  float alpha = 1.f;
+  int32_t operand = 0;            // DOP_ADD: input index >= 1
+};
+
+struct Step {
+  int first_layer = 0, last_layer = 0;
+  std::vector<HostOp> pro, epi;
+  bool has_pool = false;
+  int pool_layer = -1;
+  int kh = 0, kw = 0, sh = 0, sw = 0, ph = 0, pw = 0, is_max = 0, cip = 1;
+  Shape4 in{}, out{};
+};
+
+struct Launch {
+  Step step;
+  int32_t kernel = K_EW;
+  int src = -1;  // -1 stack input, else intermediate buffer index
+  int dst = -1;  // -1 stack output, else intermediate buffer index
+  // pool geometry (kernels 2/3)
+  int32_t G = 1, gw = 32, Jg = 1, n_cc = 1, rows_per_task = 1, n_rb = 1, U = 1;
+  int32_t block = 256;
+  int32_t blocks_per_sm = 0;
+  bs_launch_info info{};
+};
+
+}  // namespace
+
+struct bs_plan {
+  int device = 0;
+  bool host_only = false;
+  int num_sms = 148;
+  bs_plan_info info{};
+  std::vector<Launch> launches;
+  float2* params = nullptr;            // device parameter block
+  float* inter[2] = {nullptr, nullptr};  // intermediates between serialised sequences
+  cudaStream_t copy_stream[2] = {nullptr, nullptr};  // bs_execute_host pipelines
+  cudaEvent_t ev_pool[64] = {};
+  int n_events = 0;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- a1: validation + shapes
+bs_status validate_and_shape(const bs_layer_desc* L, int n, bs_shape in, std::vector<Shape4>& shapes,
+                             int& n_inputs) {
+  if (in.n < 1 || in.c < 1 || in.h < 1 || in.w < 1)
+    return fail(BS_ERR_INVALID_ARGUMENT, "input shape (%lld,%lld,%lld,%lld) has a dimension < 1",
+                (long long)in.n, (long long)in.c, (long long)in.h, (long long)in.w);
+  shapes.assign(1, Shape4{in.n, in.c, in.h, in.w});
+  int max_operand = 0;
+  for (int i = 0; i < n; ++i) {
+    const bs_layer_desc& d = L[i];
+    Shape4 s = shapes.back();
+    switch (d.kind) {
+      case BS_OP_BATCHNORM:
+        if (!d.gamma || !d.beta || !d.running_mean || !d.running_var)
+          return fail(BS_ERR_VALIDATION, "layer %d (batchnorm): NULL parameter array", i);
+        if (!(d.eps > 0.f)) return fail(BS_ERR_VALIDATION, "layer %d (batchnorm): eps=%g must be > 0", i, d.eps);
+        for (int64_t c = 0; c < s.c; ++c)
+          if (!(d.running_var[c] >= 0.f))
+            return fail(BS_ERR_VALIDATION, "layer %d (batchnorm): running_var[%lld]=%g < 0", i, (long long)c,
+                        d.running_var[c]);
+        break;
+      case BS_OP_RELU:
+      case BS_OP_COPY:
+      case BS_OP_SCALE:
+        break;
+      case BS_OP_ADD:
+        if (d.operand < 1) return fail(BS_ERR_VALIDATION, "layer %d (add): operand=%d must be >= 1", i, d.operand);
+        max_operand = std::max(max_operand, d.operand);
+        break;
+      case BS_OP_MAXPOOL:
+      case BS_OP_AVGPOOL: {
+        const char* nm = kind_name(d.kind);
+        if (d.kernel_h < 1 || d.kernel_w < 1)
+          return fail(BS_ERR_VALIDATION, "layer %d (%s): kernel %dx%d must be >= 1", i, nm, d.kernel_h, d.kernel_w);
+        if (d.stride_h < 1 || d.stride_w < 1)
+          return fail(BS_ERR_VALIDATION, "layer %d (%s): stride %dx%d must be >= 1", i, nm, d.stride_h, d.stride_w);
+        if (d.pad_h < 0 || d.pad_w < 0 || 2 * d.pad_h > d.kernel_h || 2 * d.pad_w > d.kernel_w)
+          return fail(BS_ERR_VALIDATION, "layer %d (%s): padding %dx%d must be in [0, kernel/2]", i, nm, d.pad_h,
+                      d.pad_w);
+        const int64_t ho = (s.h + 2 * d.pad_h - d.kernel_h) < 0 ? 0 : (s.h + 2 * d.pad_h - d.kernel_h) / d.stride_h + 1;
+        const int64_t wo = (s.w + 2 * d.pad_w - d.kernel_w) < 0 ? 0 : (s.w + 2 * d.pad_w - d.kernel_w) / d.stride_w + 1;
+        if (ho < 1 || wo < 1)
+          return fail(BS_ERR_VALIDATION, "layer %d (%s): output extent %lldx%lld < 1 for input %lldx%lld", i, nm,
+                      (long long)ho, (long long)wo, (long long)s.h, (long long)s.w);
+        if (d.kernel_h > 65535 || d.kernel_w > 65535 || s.h > INT32_MAX || s.w > INT32_MAX)
+          return fail(BS_ERR_PLANNING, "layer %d (%s): extents beyond the int32 index range", i, nm);
+        s.h = ho;
+        s.w = wo;
+        break;
+      }
+      case BS_OP_CONV2D:
+      case BS_OP_LINEAR:
+        return fail(BS_ERR_PLANNING,
+                    "layer %d (%s): not optimizable -- a stack holds only element-wise and pooling layers "
+                    "(PAPER.md P:L341-351, P:L973-991)",
+                    i, kind_name(d.kind));
+      default:
+        return fail(BS_ERR_INVALID_ARGUMENT, "layer %d: unknown kind %d", i, d.kind);
+    }
+    shapes.push_back(s);
+  }
+  n_inputs = 1 + max_operand;
+  // every operand index 1..max must be used by some ADD (dense numbering)
+  for (int k = 1; k <= max_operand; ++k) {
+    bool used = false;
+    for (int i = 0; i < n; ++i) used |= (L[i].kind == BS_OP_ADD && L[i].operand == k);
+    if (!used) return fail(BS_ERR_VALIDATION, "add operands must be numbered 1..%d densely; %d unused", max_operand, k);
+  }
+  return BS_OK;
+}
+
+// ---------------------------------------------------------------- a2: layer -> op (+ BN fold)
+// BN folding in fp64, one rounding to fp32 each (north_star "BatchNorm as per-channel affine").
+HostOp fold_bn(const bs_layer_desc& d, int layer, int64_t C) {
+  HostOp op;
+  op.kind = DOP_AFFINE;
+  op.layer = layer;
+  op.affine.resize((size_t)C);
+  for (int64_t c = 0; c < C; ++c) {
+    const double scale = (double)d.gamma[c] / std::sqrt((double)d.running_var[c] + (double)d.eps);
+    const double shift = (double)d.beta[c] - (double)d.running_mean[c] * scale;
+    op.affine[(size_t)c] = make_float2((float)scale, (float)shift);
+  }
+  return op;
+}
+
+// ---------------------------------------------------------------- a3: step grouping
+// Greedy, left to right (the prose rule; the listing lst:collapse
+// P:L475-484 is inverted -- SURVEY G1): an element-wise op always joins the current step
+// (prologue before its pool, epilogue after); a pool joins iff the step has none yet,
+// otherwise it opens a new step.  A prologue/epilogue longer than kMaxOps also opens a step.
+void group_steps(const bs_layer_desc* L, int n, const std::vector<Shape4>& shapes, std::vector<Step>& steps) {
+  steps.clear();
+  Step cur;
+  cur.first_layer = 0;
+  cur.in = shapes[0];
+  bool open = false;
+  auto close = [&](int last) {
+    cur.last_layer = last;
+    steps.push_back(cur);
+    cur = Step();
+  };
+  for (int i = 0; i < n; ++i) {
+    const bs_layer_desc& d = L[i];
+    if (!open) {
+      cur.first_layer = i;
+      cur.in = shapes[i];
+      open = true;
+    }
+    if (is_pool(d.kind)) {
+      if (cur.has_pool) {
+        close(i - 1);
+        cur.first_layer = i;
+        cur.in = shapes[i];
+      }
+      cur.has_pool = true;
+      cur.pool_layer = i;
+      cur.kh = d.kernel_h; cur.kw = d.kernel_w;
+      cur.sh = d.stride_h; cur.sw = d.stride_w;
+      cur.ph = d.pad_h;    cur.pw = d.pad_w;
+      cur.is_max = d.kind == BS_OP_MAXPOOL;
+      cur.cip = d.count_include_pad ? 1 : 0;
+      continue;
+    }
+    if (d.kind == BS_OP_COPY) continue;  // identity (eval Dropout): elided
+    HostOp op;
+    if (d.kind == BS_OP_BATCHNORM) {
+      op = fold_bn(d, i, shapes[i].c);
+    } else {
+      op.layer = i;
+      op.kind = d.kind == BS_OP_RELU ? DOP_RELU : d.kind == BS_OP_SCALE ? DOP_SCALE : DOP_ADD;
+      op.alpha = d.alpha;
+      op.operand = d.operand;
+    }
+    std::vector<HostOp>& dst = cur.has_pool ? cur.epi : cur.pro;
+    if ((int)dst.size() == kMaxOps) {   // program full: serialise into a new step
+      close(i - 1);
+      cur.first_layer = i;
+      cur.in = shapes[i];
+      open = true;
+      cur.pro.push_back(op);
+      continue;
+    }
+    dst.push_back(op);
+  }
+  if (open) close(n - 1);
+  for (Step& s : steps) s.out = shapes[s.last_layer + 1];
+}
+
+int pick_unroll(const Step& s) {
+  if (s.kh == 7) return 1;
+  return 4;
+}
+
+// ---------------------------------------------------------------- a4: sequences + tiles
+// Sequence packing: this build executes one step per sequence
+// (multi-step on-chip sequences are NEXT-2 in SURVEY §8(f)); consecutive sequences are
+// serialised through plan-owned intermediates.  Tile geometry per step:
+//   element-wise step : flat 128-bit streaming, no tile.
+//   pool step         : a warp task = G lane groups (one plane each) x Jg output columns x
+//                       rows_per_task output rows.  The on-chip footprint of a task is the
+//                       ((U-1)*s + k) x gw register window per warp -- the B200 analogue of
+//                       the paper's "data per step x SIMD units".
+void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& o) {
+  p->launches.clear();
+  int inter_idx = 0;
+  for (size_t k = 0; k < steps.size(); ++k) {
+    Launch l;
+    l.step = steps[k];
+    l.src = k == 0 ? -1 : (int)((inter_idx + 1) % 2);
+    l.dst = k + 1 == steps.size() ? -1 : inter_idx;
+    if (k + 1 < steps.size()) inter_idx = (inter_idx + 1) % 2;
+    const Step& s = l.step;
+    if (!s.has_pool) {
+      l.kernel = K_EW;
+    } else {
+      const int64_t Wo = s.out.w, Ho = s.out.h;
+      if (s.kw > 32) {
+        l.kernel = K_POOL_NAIVE;
+      } else {
+        l.kernel = (!o.force_generic && pool_has_specialisation(s.kh, s.kw, s.sh, s.sw)) ? K_POOL_SPEC
+                                                                                         : K_POOL_GENERIC;
+        int jmax = (32 - s.kw) / s.sw + 1;
+        int Jg = (int)std::min<int64_t>(jmax, Wo);
+        if (o.force_outputs_per_group > 0) Jg = std::min(Jg, o.force_outputs_per_group);
+        // balance chunks: same number of chunks, as even as possible
+        const int n_cc = (int)((Wo + Jg - 1) / Jg);
+        Jg = (int)((Wo + n_cc - 1) / n_cc);
+        l.Jg = Jg;
+        l.n_cc = n_cc;
+        l.gw = (Jg - 1) * s.sw + s.kw;
+        l.G = 32 / l.gw;
+        l.U = l.kernel == K_POOL_SPEC ? pick_unroll(s) : 1;
+      }
+      (void)Ho;
+    }
+    p->launches.push_back(l);
+  }
+}
+
+// Row banding: enough warp tasks to fill the device several times over, bands a
+// multiple of U rows, halo re-read (k - s rows per band) kept under 1/8 of a band.
+void size_rows(const bs_plan* p, Launch& l, const bs_plan_options& o, int64_t n_planes) {
+  const Step& s = l.step;
+  const int64_t Ho = s.out.h;
+  const int64_t base_tasks = ((n_planes + l.G - 1) / l.G) * l.n_cc;
+  const int64_t resident_warps = (int64_t)p->num_sms * std::max(1, l.blocks_per_sm) * (l.block / 32);
+  int64_t rows = Ho;
+  if (o.force_rows_per_task > 0) {
+    rows = std::min<int64_t>(Ho, o.force_rows_per_task);
+  } else if (base_tasks < 8 * resident_warps) {
+    const int64_t want_rb = (8 * resident_warps + base_tasks - 1) / base_tasks;
+    rows = (Ho + want_rb - 1) / want_rb;
+    const int halo = std::max(0, s.kh - s.sh);
+    const int64_t min_rows = halo > 0 ? (8 * halo + s.sh - 1) / s.sh : 1;
+    rows = std::max<int64_t>(rows, std::max<int64_t>(min_rows, l.U));
+    rows = (rows + l.U - 1) / l.U * l.U;
+    rows = std::min<int64_t>(rows, Ho);
+  }
+  l.rows_per_task = (int32_t)std::max<int64_t>(1, rows);
+  l.n_rb = (int32_t)((Ho + l.rows_per_task - 1) / l.rows_per_task);
+}
+
+OpProgram make_prog(const bs_plan* p, const std::vector<HostOp>& ops) {
+  OpProgram P;
+  std::memset(&P, 0, sizeof P);
+  P.n = (int32_t)ops.size();
+  int aff = 0, add = 0;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    P.kind[i] = ops[i].kind;
+    P.alpha[i] = ops[i].alpha;
+    P.affine[i] = ops[i].kind == DOP_AFFINE && p->params ? p->params + ops[i].affine_off : nullptr;
+    P.aff_slot[i] = (ops[i].kind == DOP_AFFINE && aff < kAffSlots) ? aff++ : -1;
+    P.add_slot[i] = (ops[i].kind == DOP_ADD && add == 0) ? add++ : -1;
+  }
+  for (size_t i = ops.size(); i < (size_t)kMaxOps; ++i) {
+    P.aff_slot[i] = -1;
+    P.add_slot[i] = -1;
+  }
+  return P;
+}
+
+void fill_operands(OpProgram& P, const std::vector<HostOp>& ops, const float* const* inputs) {
+  for (size_t i = 0; i < ops.size(); ++i)
+    if (ops[i].kind == DOP_ADD) P.operand[i] = inputs[ops[i].operand];
+}
+
+PoolArgs make_pool_args(const bs_plan* p, const Launch& l) {
+  PoolArgs a;
+  std::memset(&a, 0, sizeof a);
+  const Step& s = l.step;
+  a.C = (int32_t)s.in.c;
+  a.H = (int32_t)s.in.h;
+  a.W = (int32_t)s.in.w;
+  a.Ho = (int32_t)s.out.h;
+  a.Wo = (int32_t)s.out.w;
+  a.kh = s.kh; a.kw = s.kw; a.sh = s.sh; a.sw = s.sw; a.ph = s.ph; a.pw = s.pw;
+  a.is_max = s.is_max;
+  a.count_include_pad = s.cip;
+  a.G = l.G; a.gw = l.gw; a.Jg = l.Jg; a.n_cc = l.n_cc;
+  a.rows_per_task = l.rows_per_task; a.n_rb = l.n_rb;
+  a.pro = make_prog(p, s.pro);
+  a.epi = make_prog(p, s.epi);
+  return a;
+}
+
+int64_t pool_tasks(const Launch& l, int64_t n_planes) {
+  if (l.kernel == K_POOL_NAIVE) return n_planes * l.step.out.h * l.step.out.w;
+  return ((n_planes + l.G - 1) / l.G) * l.n_cc * l.n_rb;
+}
+
+int pool_grid(const Launch& l, int64_t n_tasks) {
+  int64_t g = l.kernel == K_POOL_NAIVE ? (n_tasks + 255) / 256 : (n_tasks + 7) / 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, INT32_MAX / 2));
+}
+
+constexpr int64_t kEwMaxElems = (int64_t(1) << 31) - 1024;
+
+int ew_grid(int64_t n_elems) {
+  const int64_t per_block = 256 * 4 * 4;  // kEwBlock * kEwUnroll * 4 floats
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n_elems + per_block - 1) / per_block, INT32_MAX / 2));
+}
+
+void fill_info(bs_plan* p, const std::vector<Shape4>& shapes, int n_layers, int n_inputs) {
+  bs_plan_info& I = p->info;
+  std::memset(&I, 0, sizeof I);
+  const Shape4& o = shapes.back();
+  I.out = bs_shape{o.n, o.c, o.h, o.w};
+  I.n_layers = n_layers;
+  I.n_steps = (int32_t)p->launches.size();
+  I.n_sequences = I.n_steps;
+  I.n_launches = I.n_steps;
+  I.n_inputs = n_inputs;
+  int n_ops = 0;
+  int64_t params = 0, inter = 0;
+  for (auto& l : p->launches) {
+    n_ops += (int)(l.step.pro.size() + l.step.epi.size()) + (l.step.has_pool ? 1 : 0);
+    for (auto* v : {&l.step.pro, &l.step.epi})
+      for (auto& op : *v) params += (int64_t)op.affine.size() * 8;
+    if (l.dst >= 0) inter = std::max<int64_t>(inter, l.step.out.numel() * 4);
+  }
+  I.n_ops = n_ops;
+  I.param_bytes = params;
+  I.intermediate_bytes = p->launches.size() > 2 ? 2 * inter : inter;
+  // algorithmic bytes: one read of the stack input + every ADD operand, one write of the output
+  int64_t rd = shapes[0].numel() * 4;
+  for (auto& l : p->launches)
+    for (auto* v : {&l.step.pro, &l.step.epi})
+      for (auto& op : *v)
+        if (op.kind == DOP_ADD) rd += shapes[op.layer].numel() * 4;
+  I.alg_bytes_read = rd;
+  I.alg_bytes_written = o.numel() * 4;
+}
+
+void fill_launch_info(bs_plan* p) {
+  for (auto& l : p->launches) {
+    bs_launch_info& li = l.info;
+    std::memset(&li, 0, sizeof li);
+    const Step& s = l.step;
+    li.kernel = l.kernel;
+    li.first_layer = s.first_layer;
+    li.last_layer = s.last_layer;
+    li.in = bs_shape{s.in.n, s.in.c, s.in.h, s.in.w};
+    li.out = bs_shape{s.out.n, s.out.c, s.out.h, s.out.w};
+    if (s.has_pool) {
+      li.pool_kh = s.kh; li.pool_kw = s.kw; li.pool_sh = s.sh;
+      li.pool_sw = s.sw; li.pool_ph = s.ph; li.pool_pw = s.pw;
+    }
+    li.n_prologue_ops = (int32_t)s.pro.size();
+    li.n_epilogue_ops = (int32_t)s.epi.size();
+    li.block = 256;
+    const int64_t n_planes = s.in.n * s.in.c;
+    if (l.kernel == K_EW) {
+      li.grid = ew_grid(std::min<int64_t>(s.in.numel(), kEwMaxElems));
+      li.n_tasks = 0;
+    } else {
+      li.groups_per_warp = l.G;
+      li.outputs_per_group = l.Jg;
+      li.rows_per_task = l.rows_per_task;
+      li.halo_rows = std::max(0, s.kh - s.sh);
+      li.n_tasks = pool_tasks(l, n_planes);
+      li.grid = pool_grid(l, li.n_tasks);
+    }
+    int64_t rd = s.in.numel() * 4;
+    for (auto* v : {&s.pro, &s.epi})
+      for (auto& op : *v)
+        if (op.kind == DOP_ADD) rd += (v == &s.pro ? s.in.numel() : s.out.numel()) * 4;
+    li.alg_bytes_read = rd;
+    li.alg_bytes_written = s.out.numel() * 4;
+  }
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + nb && y < x + na;
+}
+
+// ---------------------------------------------------------------- a5: dispatch
+// Enqueue every launch for images [img0, img1) on `st`.
+bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int64_t img0, int64_t img1,
+                  cudaStream_t st) {
+  for (size_t k = 0; k < p->launches.size(); ++k) {
+    const Launch& l = p->launches[k];
+    const Step& s = l.step;
+    const float* src = l.src < 0 ? inputs[0] : p->inter[l.src];
+    float* dst = l.dst < 0 ? out : p->inter[l.dst];
+    cudaError_t e = cudaSuccess;
+    if (l.kernel == K_EW) {
+      EwArgs a;
+      std::memset(&a, 0, sizeof a);
+      a.prog = make_prog(p, s.pro);
+      fill_operands(a.prog, s.pro, inputs);
+      const int64_t CHW = s.in.c * s.in.h * s.in.w;
+      a.hw = make_fastdiv((uint32_t)(s.in.h * s.in.w));
+      a.c = make_fastdiv((uint32_t)s.in.c);
+      a.hw_ge4 = s.in.h * s.in.w >= 4;
+      // split into pieces of < 2^31 elements rebased at multiples of 4 images (16-B aligned,
+      // channel index of the local element = (e / HW) % C still holds)
+      int64_t step_imgs = std::max<int64_t>(4, (kEwMaxElems / CHW) / 4 * 4);
+      for (int64_t b = (img0 / 4) * 4; b < img1; b += step_imgs) {
+        const int64_t lo = std::max(img0, b), hi = std::min(img1, b + step_imgs);
+        if (lo >= hi) continue;
+        const int64_t off = b * CHW;
+        EwArgs q = a;
+        q.in = src + off;
+        q.out = dst + off;
+        for (int i = 0; i < q.prog.n; ++i)
+          if (q.prog.kind[i] == DOP_ADD) q.prog.operand[i] += off;
+        q.add0_ptr = nullptr;
+        for (int i = 0; i < q.prog.n; ++i)
+          if (q.prog.add_slot[i] == 0) q.add0_ptr = q.prog.operand[i];
+        q.e_begin = (lo - b) * CHW;
+        q.e_end = (hi - b) * CHW;
+        e = launch_ew(q, ew_grid(q.e_end - q.e_begin), 256, st);
+        if (e != cudaSuccess) break;
+      }
+    } else {
+      PoolArgs a = make_pool_args(p, l);
+      fill_operands(a.pro, s.pro, inputs);
+      fill_operands(a.epi, s.epi, inputs);
+      a.in = src;
+      a.out = dst;
+      a.plane0 = img0 * s.in.c;
+      a.n_planes = (img1 - img0) * s.in.c;
+      a.n_tasks = pool_tasks(l, a.n_planes);
+      e = launch_pool(a, l.kernel, pool_grid(l, a.n_tasks), 256, st);
+    }
+    if (e != cudaSuccess)
+      return fail(BS_ERR_CUDA, "launch %zu (layers %d..%d): %s", k, s.first_layer, s.last_layer,
+                  cudaGetErrorString(e));
+  }
+  return BS_OK;
+}
+
+bs_status check_exec_args(const bs_plan* p, const float* const* inputs, int32_t n_inputs, const float* out) {
+  if (!p) return fail(BS_ERR_INVALID_ARGUMENT, "plan is NULL");
+  if (p->host_only) return fail(BS_ERR_INVALID_ARGUMENT, "plan was created host_only; it cannot be executed");
+  if (!inputs || !out) return fail(BS_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
+  if (n_inputs != p->info.n_inputs)
+    return fail(BS_ERR_INVALID_ARGUMENT, "plan needs %d inputs (stack input + ADD operands), got %d",
+                p->info.n_inputs, n_inputs);
+  const size_t out_bytes = (size_t)(p->info.out.n * p->info.out.c * p->info.out.h * p->info.out.w) * 4;
+  if ((uintptr_t)out % 16) return fail(BS_ERR_INVALID_ARGUMENT, "out is not 16-byte aligned");
+  bool all_ew = true;
+  for (auto& l : p->launches) all_ew &= !l.step.has_pool;
+  const Shape4 in0 = p->launches.front().step.in;
+  for (int k = 0; k < n_inputs; ++k) {
+    if (!inputs[k]) return fail(BS_ERR_INVALID_ARGUMENT, "inputs[%d] is NULL", k);
+    if ((uintptr_t)inputs[k] % 16) return fail(BS_ERR_INVALID_ARGUMENT, "inputs[%d] is not 16-byte aligned", k);
+    size_t nb = (size_t)in0.numel() * 4;
+    if (k > 0) {   // operand k's bytes = its ADD layer's input shape
+      for (auto& l : p->launches)
+        for (auto* v : {&l.step.pro, &l.step.epi})
+          for (auto& op : *v)
+            if (op.kind == DOP_ADD && op.operand == k)
+              nb = (size_t)((v == &l.step.pro ? l.step.in : l.step.out).numel()) * 4;
+    }
+    if (overlaps(inputs[k], nb, out, out_bytes)) {
+      const bool inplace_ok = k == 0 && all_ew && p->launches.size() == 1 && (const void*)inputs[0] == (const void*)out;
+      if (!inplace_ok)
+        return fail(BS_ERR_INVALID_ARGUMENT, "out overlaps inputs[%d] (only exact in==out for element-wise plans)", k);
+    }
+  }
+  return BS_OK;
+}
+
+void free_plan(bs_plan* p) {
+  if (!p) return;
+  if (!p->host_only) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    if (p->params) cudaFree(p->params);
+    for (float* b : p->inter)
+      if (b) cudaFree(b);
+    for (auto& s : p->copy_stream)
+      if (s) cudaStreamDestroy(s);
+    for (int i = 0; i < p->n_events; ++i) cudaEventDestroy(p->ev_pool[i]);
+    cudaSetDevice(prev);
+  }
+  delete p;
+}
+
+}  // namespace
+
+// ================================================================= extern "C"
+extern "C" {
+
+int32_t bs_version(void) { return 1; }
+
+const char* bs_last_error(void) { return g_err.c_str(); }
+
+const char* bs_status_string(bs_status s) {
+  switch (s) {
+    case BS_OK: return "BS_OK";
+    case BS_ERR_INVALID_ARGUMENT: return "BS_ERR_INVALID_ARGUMENT";
+    case BS_ERR_VALIDATION: return "BS_ERR_VALIDATION";
+    case BS_ERR_PLANNING: return "BS_ERR_PLANNING";
+    case BS_ERR_CUDA: return "BS_ERR_CUDA";
+    case BS_ERR_OUT_OF_MEMORY: return "BS_ERR_OUT_OF_MEMORY";
+    default: return "BS_ERR_UNKNOWN";
+  }
+}
+
+bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape input,
+                         const bs_plan_options* opts, bs_plan** plan_out) {
+  g_err.clear();
+  if (!plan_out) return fail(BS_ERR_INVALID_ARGUMENT, "plan_out is NULL");
+  *plan_out = nullptr;
+  if (!layers || n_layers < 1) return fail(BS_ERR_INVALID_ARGUMENT, "need at least one layer (n_layers=%d)", n_layers);
+  bs_plan_options o;
+  std::memset(&o, 0, sizeof o);
+  o.device = -1;
+  if (opts) o = *opts;
+
+  std::vector<Shape4> shapes;
+  int n_inputs = 1;
+  bs_status st = validate_and_shape(layers, n_layers, input, shapes, n_inputs);
+  if (st != BS_OK) return st;
+  for (const Shape4& s : shapes)
+    if (s.n * s.c > INT32_MAX || s.h * s.w > INT32_MAX / 4 || 4 * s.c * s.h * s.w > kEwMaxElems)
+      return fail(BS_ERR_PLANNING, "tensor (%lld,%lld,%lld,%lld) exceeds the index range", (long long)s.n,
+                  (long long)s.c, (long long)s.h, (long long)s.w);
+
+  bs_plan* p = new (std::nothrow) bs_plan();
+  if (!p) return fail(BS_ERR_OUT_OF_MEMORY, "host allocation failed");
+  p->host_only = o.host_only != 0;
+  if (!p->host_only) {
+    int dev = o.device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+      delete p;
+      return fail(BS_ERR_CUDA, "cudaGetDevice failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    p->device = dev;
+    if (cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      delete p;
+      return fail(BS_ERR_CUDA, "cannot query device %d: %s", dev, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+
+  std::vector<Step> steps;
+  group_steps(layers, n_layers, shapes, steps);
+  pack_and_tile(p, steps, o);
+  for (Launch& l : p->launches) {
+    if (l.kernel != K_EW) {
+      int bps = 0;
+      if (!p->host_only) {
+        PoolArgs probe = make_pool_args(p, l);
+        bps = pool_max_blocks_per_sm(l.kernel, probe, 256);
+      }
+      l.blocks_per_sm = bps > 0 ? bps : 5;
+      if (l.kernel != K_POOL_NAIVE) size_rows(p, l, o, l.step.in.n * l.step.in.c);
+    }
+  }
+  fill_info(p, shapes, n_layers, n_inputs);
+  fill_launch_info(p);
+
+  // parameter block layout
+  size_t n_f2 = 0;
+  for (Launch& l : p->launches)
+    for (auto* v : {&l.step.pro, &l.step.epi})
+      for (HostOp& op : *v)
+        if (op.kind == DOP_AFFINE) {
+          op.affine_off = n_f2;
+          n_f2 += op.affine.size();
+        }
+
+  if (!p->host_only) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    auto cuda_fail = [&](const char* what, cudaError_t e) {
+      cudaSetDevice(prev);
+      free_plan(p);
+      return fail(e == cudaErrorMemoryAllocation ? BS_ERR_OUT_OF_MEMORY : BS_ERR_CUDA, "%s: %s", what,
+                  cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    if (n_f2) {
+      if ((e = cudaMalloc(&p->params, n_f2 * sizeof(float2))) != cudaSuccess) return cuda_fail("cudaMalloc(params)", e);
+      std::vector<float2> host(n_f2);
+      for (Launch& l : p->launches)
+        for (auto* v : {&l.step.pro, &l.step.epi})
+          for (HostOp& op : *v)
+            if (op.kind == DOP_AFFINE) std::copy(op.affine.begin(), op.affine.end(), host.begin() + op.affine_off);
+      if ((e = cudaMemcpy(p->params, host.data(), n_f2 * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_fail("cudaMemcpy(params)", e);
+    }
+    int64_t inter = 0;
+    for (auto& l : p->launches)
+      if (l.dst >= 0) inter = std::max<int64_t>(inter, l.step.out.numel());
+    if (inter > 0) {
+      if ((e = cudaMalloc(&p->inter[0], (size_t)inter * 4)) != cudaSuccess) return cuda_fail("cudaMalloc(intermediate)", e);
+      if (p->launches.size() > 2 && (e = cudaMalloc(&p->inter[1], (size_t)inter * 4)) != cudaSuccess)
+        return cuda_fail("cudaMalloc(intermediate)", e);
+    }
+    for (auto& s : p->copy_stream)
+      if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail("cudaStreamCreate", e);
+    p->n_events = 64;
+    for (int i = 0; i < p->n_events; ++i)
+      if ((e = cudaEventCreateWithFlags(&p->ev_pool[i], cudaEventDisableTiming)) != cudaSuccess) {
+        p->n_events = i;
+        return cuda_fail("cudaEventCreate", e);
+      }
+    cudaSetDevice(prev);
+  }
+  *plan_out = p;
+  return BS_OK;
+}
+
+bs_status bs_plan_query(const bs_plan* plan, bs_plan_info* info) {
+  if (!plan || !info) return fail(BS_ERR_INVALID_ARGUMENT, "NULL argument");
+  *info = plan->info;
+  return BS_OK;
+}
+
+bs_status bs_plan_query_launch(const bs_plan* plan, int32_t index, bs_launch_info* info) {
+  if (!plan || !info) return fail(BS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (index < 0 || index >= (int32_t)plan->launches.size())
+    return fail(BS_ERR_INVALID_ARGUMENT, "launch index %d out of range [0,%zu)", index, plan->launches.size());
+  *info = plan->launches[(size_t)index].info;
+  return BS_OK;
+}
+
+bs_status bs_execute_ex(const bs_plan* plan, const float* const* inputs, int32_t n_inputs, float* out,
+                        bs_stream_t stream) {
+  bs_status st = check_exec_args(plan, inputs, n_inputs, out);
+  if (st != BS_OK) return st;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != plan->device) cudaSetDevice(plan->device);
+  st = enqueue(plan, inputs, out, 0, plan->launches.front().step.in.n, (cudaStream_t)stream);
+  if (prev != plan->device) cudaSetDevice(prev);
+  return st;
+}
+
+bs_status bs_execute(const bs_plan* plan, const float* in, float* out, bs_stream_t stream) {
+  const float* inputs[1] = {in};
+  return bs_execute_ex(plan, inputs, 1, out, stream);
+}
+
+bs_status bs_execute_host(const bs_plan* plan, const float* const* h_inputs, int32_t n_inputs, float* h_out,
+                          float* const* d_inputs, float* d_out, int32_t n_chunks, bs_stream_t stream) {
+  if (!h_inputs || !h_out) return fail(BS_ERR_INVALID_ARGUMENT, "NULL host pointer");
+  bs_status st = check_exec_args(plan, (const float* const*)d_inputs, n_inputs, d_out);
+  if (st != BS_OK) return st;
+  for (int k = 0; k < n_inputs; ++k)
+    if (!h_inputs[k]) return fail(BS_ERR_INVALID_ARGUMENT, "h_inputs[%d] is NULL", k);
+  const int64_t N = plan->launches.front().step.in.n;
+  if (n_chunks <= 0) n_chunks = (int32_t)std::min<int64_t>(N, 8);
+  n_chunks = (int32_t)std::min<int64_t>(n_chunks, N);
+  n_chunks = std::min(n_chunks, (plan->n_events - 2) / 2);
+  // kernels of all chunks run in order on `stream`, so plan-owned intermediates are reused safely
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != plan->device) cudaSetDevice(plan->device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  cudaStream_t h2d = plan->copy_stream[0], d2h = plan->copy_stream[1];
+  // per-image byte sizes of each input and the output
+  std::vector<int64_t> in_img(n_inputs);
+  in_img[0] = plan->launches.front().step.in.numel() / N * 4;
+  for (int k = 1; k < n_inputs; ++k) {
+    for (auto& l : plan->launches)
+      for (auto* v : {&l.step.pro, &l.step.epi})
+        for (auto& op : *v)
+          if (op.kind == DOP_ADD && op.operand == k)
+            in_img[k] = (v == &l.step.pro ? l.step.in : l.step.out).numel() / N * 4;
+  }
+  const int64_t out_img = plan->info.out.c * plan->info.out.h * plan->info.out.w * 4;
+  cudaError_t e = cudaSuccess;
+  cudaEvent_t* ev = const_cast<cudaEvent_t*>(plan->ev_pool);
+  // order the copy streams after prior work on the caller's stream
+  e = cudaEventRecord(ev[0], cs);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, ev[0], 0);
+  for (int32_t k = 0; k < n_chunks && e == cudaSuccess; ++k) {
+    const int64_t i0 = N * k / n_chunks, i1 = N * (k + 1) / n_chunks;
+    for (int q = 0; q < n_inputs && e == cudaSuccess; ++q)
+      e = cudaMemcpyAsync((char*)d_inputs[q] + i0 * in_img[q], (const char*)h_inputs[q] + i0 * in_img[q],
+                          (size_t)((i1 - i0) * in_img[q]), cudaMemcpyHostToDevice, h2d);
+    if (e != cudaSuccess) break;
+    cudaEvent_t copied = ev[2 + 2 * k], done = ev[3 + 2 * k];
+    if ((e = cudaEventRecord(copied, h2d)) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(cs, copied, 0)) != cudaSuccess) break;
+    st = enqueue(plan, (const float* const*)d_inputs, d_out, i0, i1, cs);
+    if (st != BS_OK) {
+      if (prev != plan->device) cudaSetDevice(prev);
+      return st;
+    }
+    if ((e = cudaEventRecord(done, cs)) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(d2h, done, 0)) != cudaSuccess) break;
+    e = cudaMemcpyAsync((char*)h_out + i0 * out_img, (const char*)d_out + i0 * out_img, (size_t)((i1 - i0) * out_img),
+                        cudaMemcpyDeviceToHost, d2h);
+  }
+  // the caller's stream completes only after the last device->host copy
+  if (e == cudaSuccess) e = cudaEventRecord(ev[1], d2h);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[1], 0);
+  if (prev != plan->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(BS_ERR_CUDA, "bs_execute_host: %s", cudaGetErrorString(e));
+  return BS_OK;
+}
+
+void bs_plan_destroy(bs_plan* plan) { free_plan(plan); }
+
+}  // extern "C"

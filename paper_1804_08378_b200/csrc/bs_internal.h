@@ -1,0 +1,82 @@
+// bs_internal.h -- shared between the host planner/runtime (bs_api.cpp) and the sm_100a
+// kernels (bs_kernels.cu).  Not part of the public ABI (see include/bs.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bs {
+
+// Longest element-wise op run fused into one prologue/epilogue.  Longer runs are split
+// into an extra step by the planner (a serialised sequence).
+constexpr int kMaxOps = 8;
+
+// Device-side element-wise operations (layer -> op mapping).
+enum DevOp : int32_t {
+  DOP_AFFINE = 1,  // folded inference BatchNorm: y = fmaf(x, scale[c], shift[c])
+  DOP_RELU = 2,    // y = x > 0 ? x : +0
+  DOP_SCALE = 3,   // y = alpha * x
+  DOP_ADD = 4,     // y = x + operand[idx]
+};
+
+// An element-wise program, passed by value as a kernel parameter.
+struct OpProgram {
+  int32_t n;
+  int32_t kind[kMaxOps];
+  const float2* affine[kMaxOps];   // DOP_AFFINE: device (scale, shift) per channel
+  float alpha[kMaxOps];            // DOP_SCALE
+  const float* operand[kMaxOps];   // DOP_ADD: device base of the operand tensor (set per execute)
+  int32_t aff_slot[kMaxOps];       // AFFINE ops whose params are cached in registers: 0/1, else -1
+  int32_t add_slot[kMaxOps];       // flat kernel: the first ADD's operand is prefetched (0), else -1
+};
+constexpr int kAffSlots = 2;
+
+// Magic-number unsigned division for n < 2^31 (q = (umulhi(n, m) + n) >> s).
+struct FastDiv {
+  uint32_t d, m, s;
+};
+FastDiv make_fastdiv(uint32_t d);
+
+// ---------------------------------------------------------------- element-wise step
+struct EwArgs {
+  const float* in;
+  float* out;
+  int64_t e_begin, e_end;   // element range (global flat indices; < 2^31 after rebasing)
+  FastDiv hw;               // plane size H*W
+  FastDiv c;                // channels
+  int32_t hw_ge4;           // H*W >= 4 (a float4 spans at most 2 planes)
+  const float* add0_ptr;    // operand of the prefetched ADD (add_slot 0), or nullptr
+  OpProgram prog;
+};
+
+// ---------------------------------------------------------------- pool step
+struct PoolArgs {
+  const float* in;          // stack/step input base (plane 0)
+  float* out;               // step output base (plane 0)
+  int32_t C, H, W, Ho, Wo;
+  int64_t plane0, n_planes; // planes [plane0, plane0 + n_planes) processed by this launch
+  int32_t kh, kw, sh, sw, ph, pw;
+  int32_t is_max, count_include_pad;
+  // column-walker geometry (kernels 2/3)
+  int32_t G;                // lane groups per warp (one plane each)
+  int32_t gw;               // lanes per group = (Jg - 1) * sw + kw  (<= 32)
+  int32_t Jg;               // output columns per group
+  int32_t n_cc;             // column chunks per plane = ceil(Wo / Jg)
+  int32_t rows_per_task;    // output rows per warp task
+  int32_t n_rb;             // row bands = ceil(Ho / rows_per_task)
+  int64_t n_tasks;          // ceil(n_planes / G) * n_cc * n_rb
+  OpProgram pro, epi;       // prologue (per input element), epilogue (per output element)
+};
+
+// Kernel variants (bs_launch_info.kernel).
+enum KernelKind : int32_t { K_EW = 1, K_POOL_SPEC = 2, K_POOL_GENERIC = 3, K_POOL_NAIVE = 4 };
+
+// Launchers (bs_kernels.cu).  Return the launch error (cudaSuccess on success).
+cudaError_t launch_ew(const EwArgs& a, int grid, int block, cudaStream_t st);
+cudaError_t launch_pool(const PoolArgs& a, int kernel_kind, int grid, int block, cudaStream_t st);
+// Whether a specialised (compile-time k/s) column-walker exists for this geometry.
+bool pool_has_specialisation(int kh, int kw, int sh, int sw);
+// Occupancy helpers for the planner.
+int ew_max_blocks_per_sm(int block);
+int pool_max_blocks_per_sm(int kernel_kind, const PoolArgs& a, int block);
+
+}  // namespace bs

@@ -1,0 +1,170 @@
+"""Host-side checks of the C ABI (no GPU): the library loads and exports every symbol
+include/bs.h declares; the planner (host_only plans) validates, groups steps, sizes tiles
+and counts algorithmic bytes as the paper and SURVEY.md §8 say."""
+import os
+import random
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import _util as U
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def bs():
+    from paper_1804_08378_b200 import _build
+    _build.build()
+    import paper_1804_08378_b200 as pkg
+    return pkg
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "bs.h")).read()
+    return re.findall(r"BS_API\s+[\w\s\*]+?\b(bs_\w+)\s*\(", txt)
+
+
+def test_exports_every_declared_symbol(bs):
+    syms = header_symbols()
+    assert len(syms) == 10, syms
+    out = subprocess.check_output(["nm", "-D", "--defined-only", bs.LIB_PATH]).decode()
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    for s in syms:
+        assert s in exported, s
+        assert hasattr(bs._lib, s)
+    # nothing but the ABI is exported (hidden visibility for internals)
+    assert {e for e in exported if e.startswith("bs_")} == set(syms)
+    assert bs.bs_version() == 1
+    assert bs.bs_status_string(4) == "BS_ERR_PLANNING"
+
+
+def test_sm100a_code_only(bs):
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", bs.LIB_PATH]).decode()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out), out
+
+
+def host_plan(bs, layers, shape, **opts):
+    return bs.bs_plan_create(layers, shape, {"host_only": 1, **opts})
+
+
+def test_step_grouping_paper_example(bs):
+    # lst:finalcode: step_0 = MaxPooling, BatchNorm, ReLU; step_1 = AvgPooling (+AvgNormalization)
+    shape = (1, 4, 16, 16)
+    layers = [synth.maxpool(2, 2), synth.batchnorm(4, 1), synth.relu(), synth.avgpool(2, 2), synth.batchnorm(4, 2)]
+    p = host_plan(bs, layers, shape)
+    info = bs.bs_plan_query(p)
+    assert info["n_steps"] == 2
+    l0, l1 = bs.bs_plan_query_launch(p, 0), bs.bs_plan_query_launch(p, 1)
+    assert (l0["first_layer"], l0["last_layer"], l0["n_prologue_ops"], l0["n_epilogue_ops"]) == (0, 2, 0, 2)
+    assert (l1["first_layer"], l1["last_layer"], l1["n_prologue_ops"], l1["n_epilogue_ops"]) == (3, 4, 0, 1)
+
+
+@pytest.mark.parametrize("layers,steps", [
+    ([synth.relu()], 1),
+    ([synth.relu()] * 8, 1),
+    ([synth.relu()] * 20, 3),   # > kMaxOps (8) fused ops: split into serialised steps (R6)
+    ([synth.batchnorm(3, 1), synth.relu(), synth.maxpool(2, 2)], 1),   # C1
+    ([synth.maxpool(3, 1, 1), synth.batchnorm(3, 1), synth.relu()] * 16, 16),  # §5.1 depth 16
+    ([synth.relu(), synth.copy(), synth.maxpool(3, 2), synth.maxpool(2, 2)], 2),
+])
+def test_step_counts(bs, layers, steps):
+    p = host_plan(bs, layers, (2, 3, 40, 40))
+    assert bs.bs_plan_query(p)["n_steps"] == steps
+
+
+def test_copy_is_elided(bs):
+    p = host_plan(bs, [synth.relu(), synth.copy(), synth.copy(), synth.maxpool(2, 2)], (1, 2, 8, 8))
+    assert bs.bs_plan_query(p)["n_ops"] == 2
+
+
+@pytest.mark.parametrize("wl", synth.WORKLOADS)
+def test_alg_bytes_match_survey(bs, wl):
+    """One read of the input + one write of the output."""
+    for case in synth.workload(wl):
+        p = host_plan(bs, case.layers, case.shape)
+        info = bs.bs_plan_query(p)
+        oshape = oracle.layer_shapes(case.layers, case.shape)[-1]
+        assert info["out"] == oshape
+        assert info["alg_bytes_read"] == 4 * int(np.prod(case.shape))
+        assert info["alg_bytes_written"] == 4 * int(np.prod(oshape))
+        assert info["n_launches"] == 1
+    c3 = synth.workload("vgg16")[0]
+    info = bs.bs_plan_query(host_plan(bs, c3.layers, c3.shape))
+    assert (info["alg_bytes_read"], info["alg_bytes_written"]) == (822083584, 205520896)   # 822.08 / 205.52 MB
+
+
+def test_shapes_agree_with_oracle_random(bs):
+    """Two independent implementations of the shape law / validation must agree."""
+    rng = random.Random(5)
+    for t in range(300):
+        shape = (rng.randint(1, 3), rng.randint(1, 5), rng.randint(1, 60), rng.randint(1, 60))
+        layers, n_ops = U.random_stack(rng, shape, max_depth=12, max_pools=5)
+        p = host_plan(bs, layers, shape)
+        info = bs.bs_plan_query(p)
+        assert info["out"] == oracle.layer_shapes(layers, shape, n_ops)[-1]
+        assert info["n_inputs"] == 1 + n_ops
+        for i in range(info["n_launches"]):
+            li = bs.bs_plan_query_launch(p, i)
+            if li["kernel"] in (2, 3):
+                G, J = li["groups_per_warp"], li["outputs_per_group"]
+                gw = (J - 1) * li["pool_sw"] + li["pool_kw"]
+                assert 1 <= G and G * gw <= 32
+                Ho, Wo = li["out"][2], li["out"][3]
+                assert J * -(-Wo // J) >= Wo and li["rows_per_task"] >= 1
+                assert li["halo_rows"] == max(0, li["pool_kh"] - li["pool_sh"])
+
+
+@pytest.mark.parametrize("layers,status,frag", [
+    ([synth.maxpool(3, 1, 2)], 3, "layer 0 (maxpool): padding"),
+    ([synth.relu(), synth.maxpool(9, 1)], 3, "layer 1 (maxpool): output extent"),
+    ([synth.Layer("avgpool", kernel=(2, 2), stride=(0, 1))], 3, "stride"),
+    ([synth.relu(), synth.Layer("conv2d")], 4, "layer 1 (conv2d): not optimizable"),
+    ([synth.Layer("linear")], 4, "linear"),
+    ([synth.add(0)], 3, "operand"),
+    ([synth.add(2)], 3, "densely"),
+])
+def test_validation_errors(bs, layers, status, frag):
+    with pytest.raises(bs.BsError) as e:
+        host_plan(bs, layers, (1, 2, 5, 5))
+    assert e.value.status == status
+    assert frag in str(e.value), str(e.value)
+
+
+def test_bn_validation(bs):
+    L = synth.batchnorm(2, 1)
+    L.var = np.array([1.0, -0.5], np.float32)
+    with pytest.raises(bs.BsError) as e:
+        host_plan(bs, [L], (1, 2, 3, 3))
+    assert e.value.status == 3 and "running_var[1]" in str(e.value)
+    L = synth.batchnorm(2, 1, eps=0.0)
+    with pytest.raises(bs.BsError):
+        host_plan(bs, [L], (1, 2, 3, 3))
+
+
+def test_bad_input_shape(bs):
+    with pytest.raises(bs.BsError) as e:
+        host_plan(bs, [synth.relu()], (1, 0, 3, 3))
+    assert e.value.status == 2
+
+
+def test_host_only_plan_cannot_execute(bs):
+    p = host_plan(bs, [synth.relu()], (1, 2, 3, 3))
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_execute(p, 1 << 20, 1 << 21, stream=0)
+    assert e.value.status == 2 and "host_only" in str(e.value)
+
+
+def test_tile_policy_fills_device(bs):
+    """Row banding: enough warp tasks for 148 SMs; bands are multiples of the unroll and keep
+    halo re-reads (k - s rows per band) small."""
+    for case in synth.workload("alexnet") + synth.workload("vgg16") + synth.workload("resnet50")[:1]:
+        li = bs.bs_plan_query_launch(host_plan(bs, case.layers, case.shape), 0)
+        assert li["n_tasks"] >= 148 * 40
+        if li["halo_rows"]:
+            assert li["halo_rows"] / (li["rows_per_task"] * li["pool_sh"]) <= 1 / 8 + 1e-9

@@ -1,0 +1,262 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): bit-exact for stacks of max-pool / ReLU / COPY (and the
+single-rounding SCALE / ADD), |gpu - ref| <= 1e-6 + 1e-5 |ref| with BatchNorm or AvgPool.
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests import _util as U
+
+pytestmark = pytest.mark.gpu
+
+
+def _bs():
+    import paper_1804_08378_b200 as bs
+    return bs
+
+
+def run_gpu(layers, x, ops=(), opts=None, dev="cuda:0"):
+    bs = _bs()
+    plan = bs.bs_plan_create(layers, x.shape, opts)
+    info = bs.bs_plan_query(plan)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    od = [torch.from_numpy(np.ascontiguousarray(o)).to(dev) for o in ops]
+    out = torch.full(info["out"], float("nan"), device=dev)
+    bs.bs_execute_ex(plan, [xd] + od, out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), plan
+
+
+def compare(layers, x, ops=(), opts=None, ctx=""):
+    got, plan = run_gpu(layers, x, ops, opts)
+    ref = oracle.run_bf(layers, x, ops)
+    U.check(got, ref, layers, ctx)
+    return got, plan
+
+
+# ----------------------------------------------------------------------------- fixtures / configs
+@pytest.mark.parametrize("case", U.load_golden(), ids=lambda c: c[0])
+def test_golden_gpu(case, cuda_dev, oracle_lib):
+    name, layers, x, ops, exp, cite = case
+    got, _ = run_gpu(layers, x, ops)
+    U.assert_bitexact(got, exp, f"{name} ({cite})")
+
+
+@pytest.mark.parametrize("wl", synth.WORKLOADS)
+def test_baseline_configs_reduced_batch(wl, cuda_dev, oracle_lib):
+    """Every stack of every BASELINE.json config at batch 2 (full C, H, W), all elements."""
+    cases = synth.workload(wl, batch=2)
+    if wl == "densenet121":   # 121 stacks: every distinct (layers, shape) kind, a spread of sizes
+        cases = cases[:3] + cases[3:-1:9] + cases[-2:]
+    for case in cases:
+        x = synth.uniform_np(case.input_seed, int(np.prod(case.shape))).reshape(case.shape)
+        compare(case.layers, x, ctx=case.name)
+
+
+def test_c1_full(cuda_dev, oracle_lib):
+    case = synth.workload("c1")[0]
+    x = synth.uniform_np(case.input_seed, int(np.prod(case.shape))).reshape(case.shape)
+    got, plan = compare(case.layers, x, ctx="c1")
+    assert got.shape == (1, 16, 16, 16)
+
+
+@pytest.mark.parametrize("wl", ["alexnet", "vgg16", "resnet50", "densenet121"])
+def test_full_size_sampled(wl, cuda_dev, oracle_lib):
+    """BASELINE.json batch sizes in the launch configuration bench.py times; the oracle
+    checks sampled images (every image is an independent unit of the stack)."""
+    bs = _bs()
+    cases = synth.workload(wl)
+    pick = {"alexnet": [0, 1, 2], "vgg16": [0, 2], "resnet50": [0, 1, 7],
+            "densenet121": [0, 1, 60, 119, 120]}[wl]
+    for idx in pick:
+        case = cases[idx]
+        N = case.shape[0]
+        x = synth.uniform_torch(case.input_seed, case.shape, device="cuda")
+        plan = bs.bs_plan_create(case.layers, case.shape)
+        out = torch.empty(bs.bs_plan_query(plan)["out"], device="cuda")
+        bs.bs_execute(plan, x, out)
+        torch.cuda.synchronize()
+        for n in sorted({0, N // 2, N - 1}):
+            xs = x[n:n + 1].cpu().numpy()
+            ref = oracle.run_bf(case.layers, xs)
+            U.check(out[n:n + 1].cpu().numpy(), ref, case.layers, f"{case.name} image {n}")
+        assert torch.isfinite(out).all()
+        del x, out
+
+
+# ----------------------------------------------------------------------------- geometry coverage
+ODD = [1, 2, 3, 5, 7, 13, 27, 55]
+
+
+@pytest.mark.parametrize("pool", [(2, 2, 0), (3, 2, 0), (3, 2, 1), (3, 1, 1), (7, 7, 0), (2, 1, 1), (5, 3, 2),
+                                  (1, 2, 0), (4, 4, 1)])
+@pytest.mark.parametrize("kind", ["maxpool", "avgpool"])
+def test_odd_shapes(pool, kind, cuda_dev, oracle_lib):
+    k, s, p = pool
+    rng = random.Random(k * 100 + s * 10 + p)
+    n = 0
+    for H in ODD:
+        for W in ODD:
+            if H + 2 * p < k or W + 2 * p < k:
+                continue
+            shape = (2, 3, H, W)
+            L = (synth.maxpool if kind == "maxpool" else synth.avgpool)(k, s, p)
+            L.count_include_pad = rng.random() < 0.5
+            layers = [synth.batchnorm(3, 777 + H, signed_gamma=True), synth.relu() if rng.random() < .5 else synth.copy(), L]
+            x = synth.uniform_np(H * 100 + W, int(np.prod(shape))).reshape(shape)
+            compare(layers, x, ctx=f"{kind} k{k}s{s}p{p} {H}x{W}")
+            for g in (0, 1):
+                compare(layers, x, opts={"force_generic": g, "force_rows_per_task": rng.randint(1, 5)},
+                        ctx=f"{kind} k{k}s{s}p{p} {H}x{W} generic={g}")
+            n += 1
+    assert n > 0
+
+
+def test_padding_hazard_negative_gamma(cuda_dev, oracle_lib):
+    """H5: BN with negative gamma before a padded max-pool must not see +inf from padding."""
+    shape = (4, 8, 17, 23)
+    x = synth.uniform_np(5, int(np.prod(shape))).reshape(shape)
+    L = synth.batchnorm(8, 31, signed_gamma=True)
+    for p in (synth.maxpool(3, 2, 1), synth.maxpool(3, 1, 1), synth.avgpool(3, 2, 1)):
+        got, _ = compare([L, p], x, ctx=p.kind)
+        assert np.all(np.isfinite(got))
+
+
+def test_tile_invariance(cuda_dev, oracle_lib):
+    """The output must not depend on the tiling: bit-identical across forced tiles."""
+    shape = (3, 5, 55, 55)
+    x = synth.uniform_np(9, int(np.prod(shape))).reshape(shape)
+    for layers in ([synth.relu(), synth.maxpool(3, 2)],
+                   [synth.batchnorm(5, 1), synth.relu(), synth.maxpool(3, 2, 1)],
+                   [synth.batchnorm(5, 2), synth.relu(), synth.avgpool(2, 2), synth.scale(0.5)]):
+        ref, _ = run_gpu(layers, x)
+        for opts in ({"force_rows_per_task": 1}, {"force_rows_per_task": 3}, {"force_rows_per_task": 7},
+                     {"force_outputs_per_group": 1}, {"force_outputs_per_group": 5},
+                     {"force_generic": 1}, {"force_generic": 1, "force_outputs_per_group": 3}):
+            got, _ = run_gpu(layers, x, opts=opts)
+            U.assert_bitexact(got, ref, f"{[L.kind for L in layers]} {opts}")
+
+
+@pytest.mark.parametrize("trial", range(60))
+def test_random_stacks(trial, cuda_dev, oracle_lib):
+    rng = random.Random(4000 + trial)
+    shape = (rng.randint(1, 3), rng.randint(1, 6), rng.randint(1, 40), rng.randint(1, 40))
+    layers, n_ops = U.random_stack(rng, shape, max_depth=rng.choice([3, 8, 20]),
+                                   max_pools=rng.choice([1, 2, 4]), seed_base=60000 + 50 * trial)
+    shapes = oracle.layer_shapes(layers, shape, n_ops)
+    x, ops = U.make_inputs(layers, shape, n_ops, 123 + trial, shapes)
+    compare(layers, x, ops, ctx=f"trial {trial} {[L.kind for L in layers]} {shape}")
+
+
+def test_multi_sequence_stack(cuda_dev, oracle_lib):
+    """Several pools -> several steps -> serialised sequences through plan intermediates."""
+    bs = _bs()
+    shape = (2, 4, 64, 48)
+    layers = []
+    for b in range(5):   # §5.1 block: MaxPool3x3/s1/p1 -> BN -> ReLU
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(4, 100 + b), synth.relu()]
+    layers += [synth.maxpool(2, 2), synth.avgpool(3, 2, 1)]
+    x = synth.uniform_np(77, int(np.prod(shape))).reshape(shape)
+    got, plan = compare(layers, x, ctx="multi")
+    info = bs.bs_plan_query(plan)
+    assert info["n_steps"] == 7 and info["n_launches"] == 7
+
+
+def test_long_elementwise_runs_split(cuda_dev, oracle_lib):
+    shape = (2, 3, 9, 11)
+    layers = [synth.scale(1.5), synth.relu(), synth.scale(-0.5)] * 6 + [synth.maxpool(2, 2)] + \
+             [synth.relu(), synth.scale(3.0)] * 5
+    x = synth.uniform_np(1, int(np.prod(shape))).reshape(shape)
+    compare(layers, x, ctx="long")
+
+
+# ----------------------------------------------------------------------------- ADD operands
+def test_residual_add_stacks(cuda_dev, oracle_lib):
+    """NEXT-1 shape: BN -> ADD -> ReLU (ResNet bottleneck tail) and ADD around a pool."""
+    for shape in [(4, 16, 14, 14), (3, 7, 13, 9), (2, 3, 1, 5)]:
+        C = shape[1]
+        layers = [synth.batchnorm(C, 5), synth.add(1), synth.relu()]
+        shapes = oracle.layer_shapes(layers, shape, 1)
+        x, ops = U.make_inputs(layers, shape, 1, 3, shapes)
+        compare(layers, x, ops, ctx=f"bn-add-relu {shape}")
+        layers = [synth.add(1), synth.relu(), synth.maxpool(3, 2, 1), synth.scale(2.0), synth.add(2)]
+        shapes = oracle.layer_shapes(layers, shape, 2)
+        x, ops = U.make_inputs(layers, shape, 2, 4, shapes)
+        compare(layers, x, ops, ctx=f"add-pool-add {shape}")
+
+
+# ----------------------------------------------------------------------------- host path / API
+def test_execute_host_matches_device(cuda_dev, oracle_lib):
+    bs = _bs()
+    for layers, shape, nops in [([synth.batchnorm(6, 1), synth.relu(), synth.maxpool(3, 2, 1)], (7, 6, 21, 19), 0),
+                                ([synth.batchnorm(5, 2), synth.add(1), synth.relu()], (9, 5, 7, 7), 1)]:
+        shapes = oracle.layer_shapes(layers, shape, nops)
+        x, ops = U.make_inputs(layers, shape, nops, 11, shapes)
+        plan = bs.bs_plan_create(layers, shape)
+        info = bs.bs_plan_query(plan)
+        h_in = [torch.from_numpy(a).pin_memory() for a in [x] + ops]
+        h_out = torch.empty(info["out"]).pin_memory()
+        d_in = [torch.empty_like(t, device="cuda") for t in h_in]
+        d_out = torch.empty(info["out"], device="cuda")
+        for chunks in (0, 1, 3, 100):
+            h_out.fill_(float("nan"))
+            bs.bs_execute_host(plan, h_in, h_out, d_in, d_out, chunks)
+            torch.cuda.synchronize()
+            U.check(h_out.numpy(), oracle.run_bf(layers, x, ops), layers, f"host chunks={chunks}")
+
+
+def test_inplace_elementwise(cuda_dev, oracle_lib):
+    bs = _bs()
+    shape = (2, 6, 13, 13)
+    layers = [synth.batchnorm(6, 8), synth.relu()]
+    x = synth.uniform_np(2, int(np.prod(shape))).reshape(shape)
+    plan = bs.bs_plan_create(layers, shape)
+    t = torch.from_numpy(x.copy()).cuda()
+    bs.bs_execute(plan, t, t)
+    torch.cuda.synchronize()
+    U.check(t.cpu().numpy(), oracle.run_bf(layers, x), layers, "inplace")
+
+
+def test_argument_errors(cuda_dev):
+    bs = _bs()
+    shape = (2, 4, 8, 8)
+    plan = bs.bs_plan_create([synth.relu(), synth.maxpool(2, 2)], shape)
+    x = torch.zeros(shape, device="cuda")
+    out = torch.zeros((2, 4, 4, 4), device="cuda")
+    big = torch.zeros(1000, device="cuda")
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_execute(plan, big.data_ptr() + 4, out)          # misaligned
+    assert e.value.status == 2
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_execute(plan, x, x)                             # overlap (pool plan: no in-place)
+    assert e.value.status == 2
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_execute_ex(plan, [x, x], out)                   # wrong input count
+    assert e.value.status == 2
+    hp = bs.bs_plan_create([synth.relu()], shape, {"host_only": 1})
+    with pytest.raises(bs.BsError):
+        bs.bs_execute(hp, x, x)
+    bs.bs_execute(plan, x, out)
+    torch.cuda.synchronize()
+
+
+def test_ew_large_tensor_rebasing(cuda_dev, oracle_lib):
+    """> 2^31 elements: the element-wise launcher splits at 4-image boundaries."""
+    bs = _bs()
+    shape = (36, 64, 1024, 1024)  # 2.4e9 elements, 9.7 GB per tensor
+    C = shape[1]
+    layers = [synth.batchnorm(C, 3), synth.relu()]
+    plan = bs.bs_plan_create(layers, shape)
+    x = synth.uniform_torch(4242, shape, device="cuda")
+    bs.bs_execute(plan, x, x)   # in place
+    torch.cuda.synchronize()
+    for n in (0, 17, 35):
+        # regenerate image n only
+        xs = synth.uniform_np(4242, C * 1024 * 1024, start=n * C * 1024 * 1024).reshape(1, C, 1024, 1024)
+        U.check(x[n:n + 1].cpu().numpy(), oracle.run_bf(layers, xs), layers, f"image {n}")
