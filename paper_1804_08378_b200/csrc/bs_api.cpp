@@ -88,6 +88,8 @@ struct Launch {
   int32_t G = 1, gw = 32, Jg = 1, n_cc = 1, rows_per_task = 1, n_rb = 1, U = 1;
   int32_t block = 256;
   int32_t blocks_per_sm = 0;
+  bool deferred = false;            // max pool: monotone prologue moved after the pool
+  std::vector<HostOp> dev_pro, dev_epi;  // programs as the kernel runs them
   bs_launch_info info{};
 };
 
@@ -257,9 +259,34 @@ void group_steps(const bs_layer_desc* L, int n, const std::vector<Shape4>& shape
   for (Step& s : steps) s.out = shapes[s.last_layer + 1];
 }
 
-int pick_unroll(const Step& s) {
-  if (s.kh == 7) return 1;
-  return 4;
+bool monotone(const HostOp& op) { return op.kind == DOP_AFFINE || op.kind == DOP_RELU || op.kind == DOP_SCALE; }
+
+int32_t prog_class(const std::vector<HostOp>& ops) {
+  if (ops.empty()) return PC_NONE;
+  if (ops.size() == 1 && ops[0].kind == DOP_RELU) return PC_RELU;
+  if (ops.size() == 1 && ops[0].kind == DOP_AFFINE) return PC_AFFINE;
+  if (ops.size() == 2 && ops[0].kind == DOP_AFFINE && ops[1].kind == DOP_RELU) return PC_AFFINE_RELU;
+  return PC_GENERIC;
+}
+
+// Decide the programs the kernel runs.  Max pools on the column walkers defer a monotone
+// prologue past the pool (bit-exact, bs_kernels.cu header; R5).
+void set_device_programs(Launch& l) {
+  const Step& s = l.step;
+  l.dev_pro = s.pro;
+  l.dev_epi = s.epi;
+  l.deferred = false;
+  if (!s.has_pool || !s.is_max || l.kernel == K_POOL_NAIVE) return;
+  bool ok = s.pro.size() + s.epi.size() <= (size_t)kMaxOps;
+  for (const HostOp& op : s.pro) ok = ok && monotone(op);
+  if (ok) {
+    l.dev_epi = s.pro;
+    l.dev_epi.insert(l.dev_epi.end(), s.epi.begin(), s.epi.end());
+    l.dev_pro.clear();
+    l.deferred = true;
+  } else if (l.kernel == K_POOL_SPEC && !s.pro.empty()) {
+    l.kernel = K_POOL_GENERIC;   // per-element prologue on a max pool: runtime-geometry walker
+  }
 }
 
 // ---------------------------------------------------------------- a4: sequences + tiles
@@ -300,10 +327,12 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
         l.n_cc = n_cc;
         l.gw = (Jg - 1) * s.sw + s.kw;
         l.G = 32 / l.gw;
-        l.U = l.kernel == K_POOL_SPEC ? pick_unroll(s) : 1;
+        l.U = l.kernel == K_POOL_SPEC ? pool_spec_unroll(s.kh, s.sh) : 1;
       }
       (void)Ho;
     }
+    set_device_programs(l);
+    if (l.kernel == K_POOL_GENERIC) l.U = 1;
     p->launches.push_back(l);
   }
 }
@@ -331,10 +360,11 @@ void size_rows(const bs_plan* p, Launch& l, const bs_plan_options& o, int64_t n_
   l.n_rb = (int32_t)((Ho + l.rows_per_task - 1) / l.rows_per_task);
 }
 
-OpProgram make_prog(const bs_plan* p, const std::vector<HostOp>& ops) {
+OpProgram make_prog(const bs_plan* p, const std::vector<HostOp>& ops, int n_deferred = 0) {
   OpProgram P;
   std::memset(&P, 0, sizeof P);
   P.n = (int32_t)ops.size();
+  P.n_deferred = n_deferred;
   int aff = 0, add = 0;
   for (size_t i = 0; i < ops.size(); ++i) {
     P.kind[i] = ops[i].kind;
@@ -369,8 +399,10 @@ PoolArgs make_pool_args(const bs_plan* p, const Launch& l) {
   a.count_include_pad = s.cip;
   a.G = l.G; a.gw = l.gw; a.Jg = l.Jg; a.n_cc = l.n_cc;
   a.rows_per_task = l.rows_per_task; a.n_rb = l.n_rb;
-  a.pro = make_prog(p, s.pro);
-  a.epi = make_prog(p, s.epi);
+  a.pro = make_prog(p, l.dev_pro);
+  a.epi = make_prog(p, l.dev_epi, l.deferred ? (int)s.pro.size() : 0);
+  a.pro_class = prog_class(l.dev_pro);
+  a.epi_class = prog_class(l.dev_epi);
   return a;
 }
 
@@ -480,6 +512,7 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       EwArgs a;
       std::memset(&a, 0, sizeof a);
       a.prog = make_prog(p, s.pro);
+      a.prog_class = prog_class(s.pro);
       fill_operands(a.prog, s.pro, inputs);
       const int64_t CHW = s.in.c * s.in.h * s.in.w;
       a.hw = make_fastdiv((uint32_t)(s.in.h * s.in.w));
@@ -507,8 +540,8 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       }
     } else {
       PoolArgs a = make_pool_args(p, l);
-      fill_operands(a.pro, s.pro, inputs);
-      fill_operands(a.epi, s.epi, inputs);
+      fill_operands(a.pro, l.dev_pro, inputs);
+      fill_operands(a.epi, l.dev_epi, inputs);
       a.in = src;
       a.out = dst;
       a.plane0 = img0 * s.in.c;
@@ -631,6 +664,15 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
 
   std::vector<Step> steps;
   group_steps(layers, n_layers, shapes, steps);
+  // parameter block layout (before the launches copy the programs)
+  size_t n_f2 = 0;
+  for (Step& st_ : steps)
+    for (auto* v : {&st_.pro, &st_.epi})
+      for (HostOp& op : *v)
+        if (op.kind == DOP_AFFINE) {
+          op.affine_off = n_f2;
+          n_f2 += op.affine.size();
+        }
   pack_and_tile(p, steps, o);
   for (Launch& l : p->launches) {
     if (l.kernel != K_EW) {
@@ -645,16 +687,6 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
   }
   fill_info(p, shapes, n_layers, n_inputs);
   fill_launch_info(p);
-
-  // parameter block layout
-  size_t n_f2 = 0;
-  for (Launch& l : p->launches)
-    for (auto* v : {&l.step.pro, &l.step.epi})
-      for (HostOp& op : *v)
-        if (op.kind == DOP_AFFINE) {
-          op.affine_off = n_f2;
-          n_f2 += op.affine.size();
-        }
 
   if (!p->host_only) {
     int prev = 0;

@@ -18,9 +18,15 @@ enum DevOp : int32_t {
   DOP_ADD = 4,     // y = x + operand[idx]
 };
 
+// Program classes: the kernels are specialised for the programs the paper's networks use
+// (ReLU; folded BN -> ReLU) and fall back to an op-outer interpreter otherwise.
+enum ProgClass : int32_t { PC_NONE = 0, PC_RELU = 1, PC_AFFINE = 2, PC_AFFINE_RELU = 3, PC_GENERIC = 4 };
+
 // An element-wise program, passed by value as a kernel parameter.
 struct OpProgram {
   int32_t n;
+  int32_t n_deferred;              // max pools: the first n_deferred ops are the (monotone)
+                                   // prologue applied after the pool (bs_kernels.cu header)
   int32_t kind[kMaxOps];
   const float2* affine[kMaxOps];   // DOP_AFFINE: device (scale, shift) per channel
   float alpha[kMaxOps];            // DOP_SCALE
@@ -45,6 +51,7 @@ struct EwArgs {
   FastDiv c;                // channels
   int32_t hw_ge4;           // H*W >= 4 (a float4 spans at most 2 planes)
   const float* add0_ptr;    // operand of the prefetched ADD (add_slot 0), or nullptr
+  int32_t prog_class;       // ProgClass of prog
   OpProgram prog;
 };
 
@@ -64,6 +71,7 @@ struct PoolArgs {
   int32_t rows_per_task;    // output rows per warp task
   int32_t n_rb;             // row bands = ceil(Ho / rows_per_task)
   int64_t n_tasks;          // ceil(n_planes / G) * n_cc * n_rb
+  int32_t pro_class, epi_class;  // ProgClass of pro / epi
   OpProgram pro, epi;       // prologue (per input element), epilogue (per output element)
 };
 
@@ -76,7 +84,9 @@ cudaError_t launch_pool(const PoolArgs& a, int kernel_kind, int grid, int block,
 // Whether a specialised (compile-time k/s) column-walker exists for this geometry.
 bool pool_has_specialisation(int kh, int kw, int sh, int sw);
 // Occupancy helpers for the planner.
-int ew_max_blocks_per_sm(int block);
+int ew_max_blocks_per_sm(int prog_class);
+// Output rows per iteration (U) of the specialised column walker for a k x k / s window.
+int pool_spec_unroll(int k, int s);
 int pool_max_blocks_per_sm(int kernel_kind, const PoolArgs& a, int block);
 
 }  // namespace bs

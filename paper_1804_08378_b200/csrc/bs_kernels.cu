@@ -3,26 +3,33 @@
 // Every kernel reads each input byte from HBM once, applies the whole step in registers
 // and writes each output byte once (§3.1; fig:trio-df P:L208-239):
 //
-//  * ew_kernel          -- a step with no pool (a6+a7+a10 collapse into one flat 128-bit
-//                          streaming pass): "directly passing the values from one
-//                          operation to another".  The paper launched one
-//                          block per channel; here the grid is flat and each
-//                          lane finds the channel of each element by magic-number division.
-//  * pool_cw_spec/_gen  -- a step [prologue | pool | epilogue] (a6-a10).  "Column walker":
-//                          a warp is split into lane groups, each owning the input columns
-//                          of a run of output columns of one (n, c) plane; the warp walks the
-//                          plane's rows, applies the prologue once per loaded element (only
-//                          to REAL elements -- padding is absent/zero in the post-prologue
-//                          domain), reduces the window vertically in registers
-//                          and horizontally with __shfl_down_sync (overlapping 3x3/s2 windows
-//                          need no shared memory and no HBM re-reads), applies the epilogue
-//                          and stores.  The paper's stacked-pool kernel used
-//                          B*C*Patches blocks with smem double buffers.
-//  * pool_naive_kernel  -- one thread per output, for windows wider than a warp.
+//  * ew_kernel<PC>       -- a step with no pool (a6+a7+a10 collapse into one flat 128-bit
+//                           streaming pass): "directly passing the values from one operation
+//                           to another".  The paper launched one block per
+//                           channel; here the grid is flat and each float4 finds
+//                           its channel by magic-number division.
+//  * pool_cw_spec<...>   -- a step [prologue | pool | epilogue] (a6-a10), "column walker":
+//                           a warp is split into lane groups, each owning the input columns of
+//                           a run of output columns of one (n, c) plane; the warp walks the
+//                           plane's rows with U*s + (k - s) independent loads in flight per
+//                           lane, reduces each window vertically in registers and horizontally
+//                           with __shfl_down_sync -- overlapping 3x3/s2 windows need no shared
+//                           memory and no HBM re-reads -- applies the epilogue and stores.
+//                           The paper's stacked-pool kernel used B*C*Patches blocks with smem
+//                           double buffers.
+//  * pool_cw_gen<...>    -- the same walk for any window geometry (runtime k, s, p).
+//  * pool_naive_kernel   -- one thread per output, for windows wider than a warp.
 //
-// Floating point: every op uses explicitly-rounded intrinsics (__fmul_rn, __fadd_rn,
-// __fmaf_rn, __fdiv_rn) so nvcc never contracts a SCALE followed by an ADD into an FMA;
-// that keeps ReLU/Max/COPY/SCALE/ADD stacks bit-exact against the oracle.
+// Max-pool prologue deferral (R5): when every prologue op is monotone (folded BN,
+// ReLU, SCALE) the host moves the prologue after the pool.  A composition of monotone
+// fp32 functions f is monotone (IEEE rounding is monotone), so max over a window of f(x) is
+// exactly f(max x) when f is non-decreasing and f(min x) when it is non-increasing; min is
+// taken as -max(-x) by flipping sign bits (exact).  Padding stays absent: only
+// loaded values are flipped.  Bit-identical to applying f per element, at 1/4 of the work.
+//
+// Floating point: explicitly-rounded intrinsics (__fmul_rn, __fadd_rn, __fmaf_rn,
+// __fdiv_rn) everywhere, so no SCALE followed by ADD is contracted into an FMA; ReLU /
+// Max / COPY / SCALE / ADD stacks stay bit-exact against the oracle.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -40,19 +47,20 @@ FastDiv make_fastdiv(uint32_t d) {
   return f;
 }
 
-__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
-  return (__umulhi(n, f.m) + n) >> f.s;
-}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.m) + n) >> f.s; }
+
+__device__ __forceinline__ float relu(float x) { return x > 0.f ? x : 0.f; }
+
+__device__ __forceinline__ float xorsign(float x, uint32_t m) { return __uint_as_float(__float_as_uint(x) ^ m); }
 
 // ------------------------------------------------------------------ element-wise programs
 
-// Load the per-channel (scale, shift) of the first kAffSlots AFFINE ops into registers.
+// Params of the first kAffSlots AFFINE ops of P for channel ch.
 __device__ __forceinline__ void load_affine(const OpProgram& P, int ch, float2 (&aff)[kAffSlots]) {
 #pragma unroll
   for (int k = 0; k < kAffSlots; ++k) aff[k] = make_float2(1.f, 0.f);
-#pragma unroll
-  for (int o = 0; o < kMaxOps; ++o) {
-    if (o < P.n && P.kind[o] == DOP_AFFINE) {
+  for (int o = 0; o < P.n; ++o) {
+    if (P.kind[o] == DOP_AFFINE) {
       const int s = P.aff_slot[o];
       if (s == 0) aff[0] = __ldg(P.affine[o] + ch);
       else if (s == 1) aff[1] = __ldg(P.affine[o] + ch);
@@ -60,54 +68,85 @@ __device__ __forceinline__ void load_affine(const OpProgram& P, int ch, float2 (
   }
 }
 
-__device__ __forceinline__ float2 affine_of(const OpProgram& P, const float2 (&aff)[kAffSlots],
-                                            int o, int ch) {
+__device__ __forceinline__ float2 affine_of(const OpProgram& P, const float2 (&aff)[kAffSlots], int o, int ch) {
   const int s = P.aff_slot[o];
   return s == 0 ? aff[0] : s == 1 ? aff[1] : __ldg(P.affine[o] + ch);
 }
 
-// Apply program P to one value of channel `ch` (params of cached AFFINE ops in `aff`);
-// `idx` is the flat index of the element in the tensor the ops act on (for ADD).
-__device__ __forceinline__ float apply_prog(const OpProgram& P, const float2 (&aff)[kAffSlots],
-                                            int ch, float x, int64_t idx) {
-#pragma unroll
-  for (int o = 0; o < kMaxOps; ++o) {
-    if (o < P.n) {
-      switch (P.kind[o]) {
-        case DOP_AFFINE: {
-          const float2 p = affine_of(P, aff, o, ch);
-          x = __fmaf_rn(x, p.x, p.y);
-          break;
-        }
-        case DOP_RELU: x = x > 0.f ? x : 0.f; break;
-        case DOP_SCALE: x = __fmul_rn(x, P.alpha[o]); break;
-        case DOP_ADD: x = __fadd_rn(x, __ldg(P.operand[o] + idx)); break;
-        default: break;
+// Sign-bit mask of the composite direction of the first P.n_deferred (monotone) ops.
+__device__ __forceinline__ uint32_t deferred_flip(const OpProgram& P, const float2 (&aff)[kAffSlots], int ch) {
+  uint32_t m = 0;
+  for (int o = 0; o < P.n_deferred; ++o) {
+    if (P.kind[o] == DOP_AFFINE) m ^= __float_as_uint(affine_of(P, aff, o, ch).x);
+    else if (P.kind[o] == DOP_SCALE) m ^= __float_as_uint(P.alpha[o]);
+  }
+  return m & 0x80000000u;
+}
+
+// Generic interpreter on one value (op loop is runtime; one switch per op).
+__device__ __forceinline__ float apply_generic(const OpProgram& P, const float2 (&aff)[kAffSlots], int ch, float x,
+                                               int64_t idx) {
+  for (int o = 0; o < P.n; ++o) {
+    switch (P.kind[o]) {
+      case DOP_AFFINE: {
+        const float2 p = affine_of(P, aff, o, ch);
+        x = __fmaf_rn(x, p.x, p.y);
+        break;
       }
+      case DOP_RELU: x = relu(x); break;
+      case DOP_SCALE: x = __fmul_rn(x, P.alpha[o]); break;
+      case DOP_ADD: x = __fadd_rn(x, __ldg(P.operand[o] + idx)); break;
+      default: break;
     }
   }
   return x;
 }
 
-// Same, channel params looked up per element (flat kernel's scalar head/tail).
-__device__ __forceinline__ float apply_prog_ch(const OpProgram& P, float x, uint32_t ch, uint32_t e) {
+// Program of class PC on one value.  For PC_AFFINE*, aff[0] holds op 0's params.
+template <int PC>
+__device__ __forceinline__ float apply1(const OpProgram& P, const float2 (&aff)[kAffSlots], int ch, float x,
+                                        int64_t idx) {
+  if (PC == PC_NONE) return x;
+  if (PC == PC_RELU) return relu(x);
+  if (PC == PC_AFFINE) return __fmaf_rn(x, aff[0].x, aff[0].y);
+  if (PC == PC_AFFINE_RELU) return relu(__fmaf_rn(x, aff[0].x, aff[0].y));
+  return apply_generic(P, aff, ch, x, idx);
+}
+
+// Program of class PC on an array of N values (rows r0+q of one column); values whose row is
+// outside the tensor are reset to `ident` (padding never goes through a prologue, H5).
+template <int PC, int N>
+__device__ __forceinline__ void apply_rows(const OpProgram& P, const float2 (&aff)[kAffSlots], int ch,
+                                           float (&v)[N], const bool (&ok)[N], float ident, int64_t idx0,
+                                           int stride) {
+  if (PC == PC_NONE) return;
+  if (PC == PC_GENERIC) {
+    for (int o = 0; o < P.n; ++o) {
+      const int kind = P.kind[o];
+      if (kind == DOP_AFFINE) {
+        const float2 p = affine_of(P, aff, o, ch);
 #pragma unroll
-  for (int o = 0; o < kMaxOps; ++o) {
-    if (o < P.n) {
-      switch (P.kind[o]) {
-        case DOP_AFFINE: {
-          const float2 p = __ldg(P.affine[o] + ch);
-          x = __fmaf_rn(x, p.x, p.y);
-          break;
-        }
-        case DOP_RELU: x = x > 0.f ? x : 0.f; break;
-        case DOP_SCALE: x = __fmul_rn(x, P.alpha[o]); break;
-        case DOP_ADD: x = __fadd_rn(x, __ldg(P.operand[o] + e)); break;
-        default: break;
+        for (int q = 0; q < N; ++q) v[q] = __fmaf_rn(v[q], p.x, p.y);
+      } else if (kind == DOP_RELU) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) v[q] = relu(v[q]);
+      } else if (kind == DOP_SCALE) {
+        const float al = P.alpha[o];
+#pragma unroll
+        for (int q = 0; q < N; ++q) v[q] = __fmul_rn(v[q], al);
+      } else if (kind == DOP_ADD) {
+        const float* opp = P.operand[o];
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          if (ok[q]) v[q] = __fadd_rn(v[q], __ldg(opp + idx0 + (int64_t)q * stride));
       }
     }
+  } else {
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] = apply1<PC>(P, aff, ch, v[q], 0);
   }
-  return x;
+#pragma unroll
+  for (int q = 0; q < N; ++q) v[q] = ok[q] ? v[q] : ident;
 }
 
 // ------------------------------------------------------------------ ew_kernel
@@ -115,39 +154,38 @@ __device__ __forceinline__ float apply_prog_ch(const OpProgram& P, float x, uint
 __device__ __forceinline__ float4 ld_stream4(const float* p) {
   float4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
   return r;
 }
 
 __device__ __forceinline__ void st_stream4(float* p, const float4& v) {
-  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
 
 constexpr int kEwBlock = 256;
-constexpr int kEwUnroll = 4;   // float4 per thread per iteration (64 B in flight per thread)
+constexpr int kEwUnroll = 4;  // float4 per thread per iteration (64 B in flight per thread)
 
+template <int PC>
 __global__ void __launch_bounds__(kEwBlock) ew_kernel(EwArgs a) {
   const uint32_t e_begin = (uint32_t)a.e_begin, e_end = (uint32_t)a.e_end;
   const uint32_t v_begin = (e_begin + 3u) & ~3u;
   const uint32_t v_end = (e_end & ~3u) > v_begin ? (e_end & ~3u) : v_begin;
   const uint32_t nv = (v_end - v_begin) >> 2;
   const OpProgram& P = a.prog;
-
   const uint32_t HW = a.hw.d, C = a.c.d;
-  // ---- vector body
+  const float2* aff0p = (PC == PC_AFFINE || PC == PC_AFFINE_RELU) ? P.affine[0] : nullptr;
+
   const uint32_t stride = gridDim.x * kEwBlock * kEwUnroll;
   for (uint32_t base = blockIdx.x * kEwBlock * kEwUnroll + threadIdx.x; base < nv; base += stride) {
-    float4 x[kEwUnroll];
-    float4 ad[kEwUnroll];
+    float4 x[kEwUnroll], ad[kEwUnroll];
 #pragma unroll
     for (int k = 0; k < kEwUnroll; ++k) {
       const uint32_t vi = base + k * kEwBlock;
       if (vi < nv) x[k] = ld_stream4(a.in + v_begin + 4u * vi);
     }
-    // the first ADD operand is streamed alongside the input
-    if (a.add0_ptr != nullptr) {
+    if (PC == PC_GENERIC && a.add0_ptr != nullptr) {
 #pragma unroll
       for (int k = 0; k < kEwUnroll; ++k) {
         const uint32_t vi = base + k * kEwBlock;
@@ -159,51 +197,68 @@ __global__ void __launch_bounds__(kEwBlock) ew_kernel(EwArgs a) {
       const uint32_t vi = base + k * kEwBlock;
       if (vi >= nv) continue;
       const uint32_t e = v_begin + 4u * vi;
-      // channel of each of the 4 elements
-      uint32_t ch[4];
-      const uint32_t plane = fdiv(e, a.hw);
-      const uint32_t rem = e - plane * HW;
-      const uint32_t c0 = plane - fdiv(plane, a.c) * C;
-      if (a.hw_ge4) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t c1 = (c0 + 1u == C) ? 0u : c0 + 1u;
-          ch[q] = (rem + q >= HW) ? c1 : c0;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t pq = fdiv(e + q, a.hw);
-          ch[q] = pq - fdiv(pq, a.c) * C;
-        }
-      }
       float v[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+      if (PC == PC_RELU) {
 #pragma unroll
-      for (int o = 0; o < kMaxOps; ++o) {
-        if (o < P.n) {
-          const int kind = P.kind[o];
+        for (int q = 0; q < 4; ++q) v[q] = relu(v[q]);
+      } else {
+        // channel of each element (a float4 spans at most two planes when H*W >= 4)
+        uint32_t ch[4];
+        const uint32_t plane = fdiv(e, a.hw);
+        const uint32_t rem = e - plane * HW;
+        const uint32_t c0 = plane - fdiv(plane, a.c) * C;
+        const uint32_t c1 = (c0 + 1u == C) ? 0u : c0 + 1u;
+        if (a.hw_ge4) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ch[q] = (rem + q >= HW) ? c1 : c0;
+        } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            switch (kind) {
-              case DOP_AFFINE: {
-                const float2 p = __ldg(P.affine[o] + ch[q]);
-                v[q] = __fmaf_rn(v[q], p.x, p.y);
-                break;
+            const uint32_t pq = fdiv(e + q, a.hw);
+            ch[q] = pq - fdiv(pq, a.c) * C;
+          }
+        }
+        if (PC == PC_AFFINE || PC == PC_AFFINE_RELU) {
+          const float2 p0 = __ldg(aff0p + c0);
+          float2 p[4] = {p0, p0, p0, p0};
+          if (!(a.hw_ge4 && rem + 3u < HW)) {   // straddles a plane boundary
+#pragma unroll
+            for (int q = 1; q < 4; ++q) p[q] = __ldg(aff0p + ch[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            v[q] = __fmaf_rn(v[q], p[q].x, p[q].y);
+            if (PC == PC_AFFINE_RELU) v[q] = relu(v[q]);
+          }
+        } else {  // generic: op-outer interpreter over the 4 values
+          for (int o = 0; o < P.n; ++o) {
+            const int kind = P.kind[o];
+            if (kind == DOP_AFFINE) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 pp = __ldg(P.affine[o] + ch[q]);
+                v[q] = __fmaf_rn(v[q], pp.x, pp.y);
               }
-              case DOP_RELU: v[q] = v[q] > 0.f ? v[q] : 0.f; break;
-              case DOP_SCALE: v[q] = __fmul_rn(v[q], P.alpha[o]); break;
-              case DOP_ADD: {
-                float tq;
-                if (P.add_slot[o] == 0) {
-                  const float4 t = ad[k];
-                  tq = q == 0 ? t.x : q == 1 ? t.y : q == 2 ? t.z : t.w;
-                } else {
-                  tq = __ldg(P.operand[o] + e + q);
-                }
-                v[q] = __fadd_rn(v[q], tq);
-                break;
+            } else if (kind == DOP_RELU) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) v[q] = relu(v[q]);
+            } else if (kind == DOP_SCALE) {
+              const float al = P.alpha[o];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) v[q] = __fmul_rn(v[q], al);
+            } else if (kind == DOP_ADD) {
+              if (P.add_slot[o] == 0) {
+                v[0] = __fadd_rn(v[0], ad[k].x);
+                v[1] = __fadd_rn(v[1], ad[k].y);
+                v[2] = __fadd_rn(v[2], ad[k].z);
+                v[3] = __fadd_rn(v[3], ad[k].w);
+              } else {
+                const float4 t = ld_stream4(P.operand[o] + e);
+                v[0] = __fadd_rn(v[0], t.x);
+                v[1] = __fadd_rn(v[1], t.y);
+                v[2] = __fadd_rn(v[2], t.z);
+                v[3] = __fadd_rn(v[3], t.w);
               }
-              default: break;
             }
           }
         }
@@ -218,11 +273,13 @@ __global__ void __launch_bounds__(kEwBlock) ew_kernel(EwArgs a) {
     const uint32_t nt = e_end > tail0 ? e_end - tail0 : 0u;
     const uint32_t t = threadIdx.x;
     if (t < nh + nt) {
-      uint32_t e = t < nh ? e_begin + t : tail0 + (t - nh);
+      const uint32_t e = t < nh ? e_begin + t : tail0 + (t - nh);
       if (e < e_end && !(e >= v_begin && e < v_end)) {
         const uint32_t plane = fdiv(e, a.hw);
-        const uint32_t ch = plane - fdiv(plane, a.c) * C;
-        a.out[e] = apply_prog_ch(P, a.in[e], ch, e);
+        const int ch = (int)(plane - fdiv(plane, a.c) * C);
+        float2 aff[kAffSlots];
+        load_affine(P, ch, aff);
+        a.out[e] = apply_generic(P, aff, ch, a.in[e], e);
       }
     }
   }
@@ -236,8 +293,7 @@ __device__ __forceinline__ float red(float acc, float x) {
 }
 
 // Avg-pool divisor: kh*kw with count_include_pad, else the number of real cells.
-__device__ __forceinline__ float avg_div(const PoolArgs& a, int i, int j, int kh, int kw, int sh,
-                                         int sw) {
+__device__ __forceinline__ float avg_div(const PoolArgs& a, int i, int j, int kh, int kw, int sh, int sw) {
   if (a.count_include_pad) return (float)(kh * kw);
   const int r0 = i * sh - a.ph, q0 = j * sw - a.pw;
   const int nr = min(a.H, r0 + kh) - max(0, r0);
@@ -247,73 +303,98 @@ __device__ __forceinline__ float avg_div(const PoolArgs& a, int i, int j, int kh
 
 constexpr int kPoolBlock = 256;
 
-// Specialised column walker: compile-time window (KH x KW, stride SH x SW), U output rows
-// per iteration -> (U-1)*SH + KH independent row loads in flight per lane.
-template <int KH, int KW, int SH, int SW, bool IS_MAX, int U>
+// Per-task lane geometry shared by both column walkers.
+struct LaneTask {
+  int64_t plane;
+  int c, j, i_begin, i_end;
+  bool plane_ok, col_ok, out_lane;
+};
+
+__device__ __forceinline__ LaneTask decode_task(const PoolArgs& a, int t, int g, int l, int sw) {
+  LaneTask T;
+  const int cc = t % a.n_cc;
+  const int t2 = t / a.n_cc;
+  const int rb = t2 % a.n_rb;
+  const int pg = t2 / a.n_rb;
+  const int64_t pl_local = (int64_t)pg * a.G + g;
+  T.plane_ok = (g < a.G) && (pl_local < a.n_planes);
+  T.plane = a.plane0 + (T.plane_ok ? pl_local : 0);
+  const int j0 = cc * a.Jg;
+  T.c = j0 * sw - a.pw + l;
+  T.col_ok = T.plane_ok && T.c >= 0 && T.c < a.W;
+  const int jl = l / sw;
+  T.j = j0 + jl;
+  T.out_lane = T.plane_ok && (l - jl * sw == 0) && jl < a.Jg && T.j < a.Wo;
+  T.i_begin = rb * a.rows_per_task;
+  T.i_end = min(a.Ho, T.i_begin + a.rows_per_task);
+  return T;
+}
+
+// Specialised column walker: compile-time window (KH x KW, stride SH x SW); U output rows per
+// iteration -> NR = (U-1)*SH + KH independent row loads in flight per lane.
+//   PC: class of the per-element prologue (avg pools; max pools run with it deferred, PC_NONE)
+//   OC: class of the per-output program (deferred prologue + epilogue)
+template <int KH, int KW, int SH, int SW, bool IS_MAX, int U, int PC, int OC>
 __global__ void __launch_bounds__(kPoolBlock) pool_cw_spec(PoolArgs a) {
   constexpr int NR = (U - 1) * SH + KH;
   const int lane = threadIdx.x & 31;
-  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int wg = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * (unsigned)blockDim.x) >> 5);
   const int g = lane / a.gw;
   const int l = lane - g * a.gw;
   const float ident = IS_MAX ? -CUDART_INF_F : 0.f;
-  const int64_t HW = (int64_t)a.H * a.W, HWo = (int64_t)a.Ho * a.Wo;
+  const int HW = a.H * a.W, HWo = a.Ho * a.Wo;
+  const int n_tasks = (int)a.n_tasks;
 
-  for (int64_t t = wg; t < a.n_tasks; t += nw) {
-    int64_t tt = t;
-    const int cc = (int)(tt % a.n_cc);
-    tt /= a.n_cc;
-    const int rb = (int)(tt % a.n_rb);
-    tt /= a.n_rb;
-    const int64_t pl_local = tt * a.G + g;
-    const bool plane_ok = (g < a.G) && (pl_local < a.n_planes);
-    const int64_t plane = a.plane0 + (plane_ok ? pl_local : 0);
-    const int j0 = cc * a.Jg;
-    const int c = j0 * SW - a.pw + l;
-    const bool col_ok = plane_ok && c >= 0 && c < a.W;
-    const int jl = l / SW;
-    const int j = j0 + jl;
-    const bool out_lane = plane_ok && (l - jl * SW == 0) && jl < a.Jg && j < a.Wo;
-    const int ch = (int)(plane % a.C);
+  for (int t = wg; t < n_tasks; t += nw) {
+    const LaneTask T = decode_task(a, t, g, l, SW);
+    const int ch = (int)(T.plane % a.C);
     float2 paff[kAffSlots], eaff[kAffSlots];
-    load_affine(a.pro, ch, paff);
-    load_affine(a.epi, ch, eaff);
-    const float* pin = a.in + plane * HW;
-    const int i_begin = rb * a.rows_per_task;
-    const int i_end = min(a.Ho, i_begin + a.rows_per_task);
+    if (PC == PC_AFFINE || PC == PC_AFFINE_RELU) paff[0] = __ldg(a.pro.affine[0] + ch);
+    else if (PC == PC_GENERIC) load_affine(a.pro, ch, paff);
+    if (OC == PC_AFFINE || OC == PC_AFFINE_RELU) eaff[0] = __ldg(a.epi.affine[0] + ch);
+    else if (OC == PC_GENERIC) load_affine(a.epi, ch, eaff);
+    uint32_t flip = 0;
+    if (IS_MAX && a.epi.n_deferred > 0) {
+      if (OC == PC_AFFINE || OC == PC_AFFINE_RELU) flip = __float_as_uint(eaff[0].x) & 0x80000000u;
+      else if (OC == PC_GENERIC) flip = deferred_flip(a.epi, eaff, ch);
+    }
+    const float* pin = a.in + T.plane * (int64_t)HW + (T.col_ok ? T.c : 0);
+    float* pout = a.out + T.plane * (int64_t)HWo + T.j;
+    const int64_t in_idx0 = T.plane * (int64_t)HW + T.c;
 
-    for (int i = i_begin; i < i_end; i += U) {
+    for (int i = T.i_begin; i < T.i_end; i += U) {
       const int r0 = i * SH - a.ph;
       float v[NR];
+      bool ok[NR];
 #pragma unroll
       for (int q = 0; q < NR; ++q) {
-        const int r = r0 + q;
-        v[q] = (col_ok && r >= 0 && r < a.H) ? __ldg(pin + (int64_t)r * a.W + c) : ident;
+        ok[q] = T.col_ok && (unsigned)(r0 + q) < (unsigned)a.H;
+        v[q] = ok[q] ? __ldg(pin + (r0 + q) * a.W) : ident;
       }
-      if (a.pro.n > 0) {
+      if (IS_MAX) {
+        if (flip) {
 #pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const int r = r0 + q;
-          const bool ok = col_ok && r >= 0 && r < a.H;
-          const float y = apply_prog(a.pro, paff, ch, v[q], plane * HW + (int64_t)r * a.W + c);
-          v[q] = ok ? y : ident;   // padding stays absent (max) / zero (avg): never through BN
+          for (int q = 0; q < NR; ++q) v[q] = ok[q] ? xorsign(v[q], flip) : ident;
         }
+      } else {
+        apply_rows<PC, NR>(a.pro, paff, ch, v, ok, ident, in_idx0 + (int64_t)r0 * a.W, a.W);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (i + u < i_end) {
+        if (i + u < T.i_end) {
           float acc = v[u * SH];
 #pragma unroll
           for (int q = 1; q < KH; ++q) acc = red<IS_MAX>(acc, v[u * SH + q]);
           float res = acc;
 #pragma unroll
           for (int d = 1; d < KW; ++d) res = red<IS_MAX>(res, __shfl_down_sync(0xffffffffu, acc, d));
-          if (out_lane) {
-            if (!IS_MAX) res = __fdiv_rn(res, avg_div(a, i + u, j, KH, KW, SH, SW));
-            const int64_t oidx = plane * HWo + (int64_t)(i + u) * a.Wo + j;
-            res = apply_prog(a.epi, eaff, ch, res, oidx);
-            __stcs(a.out + oidx, res);
+          if (T.out_lane) {
+            if (IS_MAX) res = xorsign(res, flip);
+            else res = __fdiv_rn(res, avg_div(a, i + u, T.j, KH, KW, SH, SW));
+            const int orow = (i + u) * a.Wo;
+            res = apply1<OC>(a.epi, eaff, ch, res, T.plane * (int64_t)HWo + orow + T.j);
+            __stcs(pout + orow, res);
           }
         }
       }
@@ -325,69 +406,57 @@ __global__ void __launch_bounds__(kPoolBlock) pool_cw_spec(PoolArgs a) {
 template <bool IS_MAX>
 __global__ void __launch_bounds__(kPoolBlock) pool_cw_gen(PoolArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int wg = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * (unsigned)blockDim.x) >> 5);
   const int g = lane / a.gw;
   const int l = lane - g * a.gw;
   const float ident = IS_MAX ? -CUDART_INF_F : 0.f;
-  const int64_t HW = (int64_t)a.H * a.W, HWo = (int64_t)a.Ho * a.Wo;
+  const int HW = a.H * a.W, HWo = a.Ho * a.Wo;
   const int kh = a.kh, kw = a.kw, sh = a.sh, sw = a.sw;
+  const int n_tasks = (int)a.n_tasks;
 
-  for (int64_t t = wg; t < a.n_tasks; t += nw) {
-    int64_t tt = t;
-    const int cc = (int)(tt % a.n_cc);
-    tt /= a.n_cc;
-    const int rb = (int)(tt % a.n_rb);
-    tt /= a.n_rb;
-    const int64_t pl_local = tt * a.G + g;
-    const bool plane_ok = (g < a.G) && (pl_local < a.n_planes);
-    const int64_t plane = a.plane0 + (plane_ok ? pl_local : 0);
-    const int j0 = cc * a.Jg;
-    const int c = j0 * sw - a.pw + l;
-    const bool col_ok = plane_ok && c >= 0 && c < a.W;
-    const int jl = l / sw;
-    const int j = j0 + jl;
-    const bool out_lane = plane_ok && (l - jl * sw == 0) && jl < a.Jg && j < a.Wo;
-    const int ch = (int)(plane % a.C);
+  for (int t = wg; t < n_tasks; t += nw) {
+    const LaneTask T = decode_task(a, t, g, l, sw);
+    const int ch = (int)(T.plane % a.C);
     float2 paff[kAffSlots], eaff[kAffSlots];
     load_affine(a.pro, ch, paff);
     load_affine(a.epi, ch, eaff);
-    const float* pin = a.in + plane * HW;
-    const int i_begin = rb * a.rows_per_task;
-    const int i_end = min(a.Ho, i_begin + a.rows_per_task);
+    const uint32_t flip = IS_MAX ? deferred_flip(a.epi, eaff, ch) : 0u;
+    const float* pin = a.in + T.plane * (int64_t)HW + (T.col_ok ? T.c : 0);
+    const int64_t in_idx0 = T.plane * (int64_t)HW + T.c;
 
-    for (int i = i_begin; i < i_end; ++i) {
+    for (int i = T.i_begin; i < T.i_end; ++i) {
       const int r0 = i * sh - a.ph;
       float acc = ident;
 #pragma unroll 4
       for (int u = 0; u < kh; ++u) {
         const int r = r0 + u;
-        if (col_ok && r >= 0 && r < a.H) {
-          float x = __ldg(pin + (int64_t)r * a.W + c);
-          x = apply_prog(a.pro, paff, ch, x, plane * HW + (int64_t)r * a.W + c);
-          acc = red<IS_MAX>(acc, x);
+        if (T.col_ok && (unsigned)r < (unsigned)a.H) {
+          float x = __ldg(pin + r * a.W);
+          x = apply_generic(a.pro, paff, ch, x, in_idx0 + (int64_t)r * a.W);
+          acc = red<IS_MAX>(acc, IS_MAX ? xorsign(x, flip) : x);
         }
       }
       float res = acc;
       for (int d = 1; d < kw; ++d) res = red<IS_MAX>(res, __shfl_down_sync(0xffffffffu, acc, d));
-      if (out_lane) {
-        if (!IS_MAX) res = __fdiv_rn(res, avg_div(a, i, j, kh, kw, sh, sw));
-        const int64_t oidx = plane * HWo + (int64_t)i * a.Wo + j;
-        res = apply_prog(a.epi, eaff, ch, res, oidx);
+      if (T.out_lane) {
+        if (IS_MAX) res = xorsign(res, flip);
+        else res = __fdiv_rn(res, avg_div(a, i, T.j, kh, kw, sh, sw));
+        const int64_t oidx = T.plane * (int64_t)HWo + (int64_t)i * a.Wo + T.j;
+        res = apply_generic(a.epi, eaff, ch, res, oidx);
         __stcs(a.out + oidx, res);
       }
     }
   }
 }
 
-// One thread per output element (windows wider than a warp).
+// One thread per output element (windows wider than a warp).  Never deferred.
 template <bool IS_MAX>
 __global__ void __launch_bounds__(kPoolBlock) pool_naive_kernel(PoolArgs a) {
   const int64_t HW = (int64_t)a.H * a.W, HWo = (int64_t)a.Ho * a.Wo;
   const int64_t total = a.n_planes * HWo;
   const float ident = IS_MAX ? -CUDART_INF_F : 0.f;
-  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
-       o += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t plane = a.plane0 + o / HWo;
     const int64_t rem = o % HWo;
     const int i = (int)(rem / a.Wo), j = (int)(rem % a.Wo);
@@ -404,13 +473,13 @@ __global__ void __launch_bounds__(kPoolBlock) pool_naive_kernel(PoolArgs a) {
         const int q = j * a.sw - a.pw + v;
         if (q < 0 || q >= a.W) continue;
         float x = __ldg(pin + (int64_t)r * a.W + q);
-        x = apply_prog(a.pro, paff, ch, x, plane * HW + (int64_t)r * a.W + q);
+        x = apply_generic(a.pro, paff, ch, x, plane * HW + (int64_t)r * a.W + q);
         acc = red<IS_MAX>(acc, x);
       }
     }
     if (!IS_MAX) acc = __fdiv_rn(acc, avg_div(a, i, j, a.kh, a.kw, a.sh, a.sw));
     const int64_t oidx = plane * HWo + rem;
-    acc = apply_prog(a.epi, eaff, ch, acc, oidx);
+    acc = apply_generic(a.epi, eaff, ch, acc, oidx);
     __stcs(a.out + oidx, acc);
   }
 }
@@ -422,29 +491,60 @@ bool pool_has_specialisation(int kh, int kw, int sh, int sw) {
   return (kh == 2 && sh == 2) || (kh == 3 && sh == 2) || (kh == 3 && sh == 1) || (kh == 7 && sh == 7);
 }
 
-template <bool M>
-static void* spec_fn(int k, int s) {
-  if (k == 2 && s == 2) return (void*)pool_cw_spec<2, 2, 2, 2, M, 4>;
-  if (k == 3 && s == 2) return (void*)pool_cw_spec<3, 3, 2, 2, M, 4>;
-  if (k == 3 && s == 1) return (void*)pool_cw_spec<3, 3, 1, 1, M, 4>;
-  if (k == 7 && s == 7) return (void*)pool_cw_spec<7, 7, 7, 7, M, 1>;
-  return nullptr;
+int pool_spec_unroll(int k, int s) {
+  if (k == 7) return 2;
+  if (s == 1) return 8;
+  return 8;
+}
+
+template <int K, int S, int U>
+static void* spec_pick(bool is_max, int pc, int oc) {
+  if (is_max) {  // prologue deferred: only the output class varies
+    switch (oc) {
+      case PC_NONE: return (void*)pool_cw_spec<K, K, S, S, true, U, PC_NONE, PC_NONE>;
+      case PC_RELU: return (void*)pool_cw_spec<K, K, S, S, true, U, PC_NONE, PC_RELU>;
+      case PC_AFFINE_RELU: return (void*)pool_cw_spec<K, K, S, S, true, U, PC_NONE, PC_AFFINE_RELU>;
+      default: return (void*)pool_cw_spec<K, K, S, S, true, U, PC_NONE, PC_GENERIC>;
+    }
+  }
+  (void)oc;
+  switch (pc) {
+    case PC_NONE: return (void*)pool_cw_spec<K, K, S, S, false, U, PC_NONE, PC_GENERIC>;
+    case PC_RELU: return (void*)pool_cw_spec<K, K, S, S, false, U, PC_RELU, PC_GENERIC>;
+    case PC_AFFINE_RELU: return (void*)pool_cw_spec<K, K, S, S, false, U, PC_AFFINE_RELU, PC_GENERIC>;
+    default: return (void*)pool_cw_spec<K, K, S, S, false, U, PC_GENERIC, PC_GENERIC>;
+  }
 }
 
 static void* pool_fn(int kind, const PoolArgs& a) {
   const bool m = a.is_max != 0;
   switch (kind) {
-    case K_POOL_SPEC: return m ? spec_fn<true>(a.kh, a.sh) : spec_fn<false>(a.kh, a.sh);
+    case K_POOL_SPEC:
+      if (m && a.pro.n > 0) return nullptr;  // max pools reach the specialised kernel deferred only
+      if (a.kh == 2 && a.sh == 2) return spec_pick<2, 2, 8>(m, a.pro_class, a.epi_class);
+      if (a.kh == 3 && a.sh == 2) return spec_pick<3, 2, 8>(m, a.pro_class, a.epi_class);
+      if (a.kh == 3 && a.sh == 1) return spec_pick<3, 1, 8>(m, a.pro_class, a.epi_class);
+      if (a.kh == 7 && a.sh == 7) return spec_pick<7, 7, 2>(m, a.pro_class, a.epi_class);
+      return nullptr;
     case K_POOL_GENERIC: return m ? (void*)pool_cw_gen<true> : (void*)pool_cw_gen<false>;
     case K_POOL_NAIVE: return m ? (void*)pool_naive_kernel<true> : (void*)pool_naive_kernel<false>;
     default: return nullptr;
   }
 }
 
+static void* ew_fn(int pc) {
+  switch (pc) {
+    case PC_RELU: return (void*)ew_kernel<PC_RELU>;
+    case PC_AFFINE: return (void*)ew_kernel<PC_AFFINE>;
+    case PC_AFFINE_RELU: return (void*)ew_kernel<PC_AFFINE_RELU>;
+    default: return (void*)ew_kernel<PC_GENERIC>;
+  }
+}
+
 cudaError_t launch_ew(const EwArgs& a, int grid, int block, cudaStream_t st) {
   (void)block;
-  ew_kernel<<<grid, kEwBlock, 0, st>>>(a);
-  return cudaGetLastError();
+  void* args[] = {(void*)&a};
+  return cudaLaunchKernel(ew_fn(a.prog_class), dim3(grid), dim3(kEwBlock), args, 0, st);
 }
 
 cudaError_t launch_pool(const PoolArgs& a, int kind, int grid, int block, cudaStream_t st) {
@@ -455,10 +555,9 @@ cudaError_t launch_pool(const PoolArgs& a, int kind, int grid, int block, cudaSt
   return cudaLaunchKernel(fn, dim3(grid), dim3(kPoolBlock), args, 0, st);
 }
 
-int ew_max_blocks_per_sm(int block) {
+int ew_max_blocks_per_sm(int pc) {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ew_kernel, kEwBlock, 0) != cudaSuccess) n = 0;
-  (void)block;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ew_fn(pc), kEwBlock, 0) != cudaSuccess) n = 0;
   return n;
 }
 
