@@ -98,8 +98,9 @@ typedef struct {
     int32_t force_rows_per_task;    /* 0 = planner; >0 forces the output-row band of a pool
                                        tile (tests use it: results must not depend on tiling) */
     int32_t force_outputs_per_group;/* 0 = planner; >0 forces output columns per lane group */
-    int32_t force_generic;          /* 1 = use the runtime-geometry pool kernel even where a
-                                       specialised one exists (tests) */
+    int32_t force_generic;          /* 0 = planner picks the pool kernel; 1 = force the
+                                       runtime-geometry column walker; 2 = never the vector
+                                       column walker (tests: results must not depend on it) */
     int32_t reserved[5];
 } bs_plan_options;
 
@@ -119,7 +120,8 @@ typedef struct {
 typedef struct {
     int32_t kernel;                 /* 1 = element-wise streaming, 2 = pool column-walker
                                        (specialised k/s), 3 = pool column-walker (runtime
-                                       geometry), 4 = pool one-thread-per-output */
+                                       geometry), 4 = pool one-thread-per-output,
+                                       5 = pool vector column walker (stride 2, W % 2 == 0) */
     int32_t first_layer, last_layer;/* layer index range [first, last] covered */
     bs_shape in, out;
     int32_t pool_kh, pool_kw, pool_sh, pool_sw, pool_ph, pool_pw;  /* 0 if no pool */

@@ -269,24 +269,26 @@ int32_t prog_class(const std::vector<HostOp>& ops) {
   return PC_GENERIC;
 }
 
-// Decide the programs the kernel runs.  Max pools on the column walkers defer a monotone
-// prologue past the pool (bit-exact, bs_kernels.cu header; R5).
+// A max pool's prologue can run after the pool when every op is monotone (bit-exact,
+// bs_kernels.cu header; R5) and the merged program fits.
+bool max_deferrable(const Step& s) {
+  if (!s.has_pool || !s.is_max) return false;
+  bool ok = s.pro.size() + s.epi.size() <= (size_t)kMaxOps;
+  for (const HostOp& op : s.pro) ok = ok && monotone(op);
+  return ok;
+}
+
+// Decide the programs the kernel runs.
 void set_device_programs(Launch& l) {
   const Step& s = l.step;
   l.dev_pro = s.pro;
   l.dev_epi = s.epi;
   l.deferred = false;
-  if (!s.has_pool || !s.is_max || l.kernel == K_POOL_NAIVE) return;
-  bool ok = s.pro.size() + s.epi.size() <= (size_t)kMaxOps;
-  for (const HostOp& op : s.pro) ok = ok && monotone(op);
-  if (ok) {
-    l.dev_epi = s.pro;
-    l.dev_epi.insert(l.dev_epi.end(), s.epi.begin(), s.epi.end());
-    l.dev_pro.clear();
-    l.deferred = true;
-  } else if (l.kernel == K_POOL_SPEC && !s.pro.empty()) {
-    l.kernel = K_POOL_GENERIC;   // per-element prologue on a max pool: runtime-geometry walker
-  }
+  if (l.kernel == K_EW || l.kernel == K_POOL_NAIVE || !max_deferrable(s)) return;
+  l.dev_epi = s.pro;
+  l.dev_epi.insert(l.dev_epi.end(), s.epi.begin(), s.epi.end());
+  l.dev_pro.clear();
+  l.deferred = true;
 }
 
 // ---------------------------------------------------------------- a4: sequences + tiles
@@ -312,11 +314,26 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
       l.kernel = K_EW;
     } else {
       const int64_t Wo = s.out.w, Ho = s.out.h;
+      const bool per_elem_max = s.is_max && !s.pro.empty() && !max_deferrable(s);
+      const int vec = pool_vec_width(s.kh, s.kw, s.sh, s.sw, s.ph, s.pw, (int)s.in.w, (int)Wo);
       if (s.kw > 32) {
         l.kernel = K_POOL_NAIVE;
+      } else if (vec && o.force_generic == 0 && !per_elem_max) {
+        // vector column walker: each lane VEC columns, VEC/2 outputs; halo lane for 3-wide windows
+        l.kernel = K_POOL_VEC;
+        const int opl = vec / 2, halo = s.kw == 3 ? 1 : 0;
+        int Jg = opl * (32 - halo);
+        if (o.force_outputs_per_group > 0) Jg = std::max(opl, std::min(Jg, o.force_outputs_per_group / opl * opl));
+        const int64_t need = (Wo + opl - 1) / opl * opl;
+        if (need <= Jg) Jg = (int)need;
+        l.Jg = Jg;
+        l.n_cc = (int)((Wo + Jg - 1) / Jg);
+        l.gw = Jg / opl + halo;
+        l.G = 32 / l.gw;
+        l.U = pool_vec_unroll(vec);
       } else {
-        l.kernel = (!o.force_generic && pool_has_specialisation(s.kh, s.kw, s.sh, s.sw)) ? K_POOL_SPEC
-                                                                                         : K_POOL_GENERIC;
+        l.kernel = (o.force_generic != 1 && !per_elem_max && pool_has_specialisation(s.kh, s.kw, s.sh, s.sw))
+                       ? K_POOL_SPEC : K_POOL_GENERIC;
         int jmax = (32 - s.kw) / s.sw + 1;
         int Jg = (int)std::min<int64_t>(jmax, Wo);
         if (o.force_outputs_per_group > 0) Jg = std::min(Jg, o.force_outputs_per_group);

@@ -76,7 +76,7 @@ struct PoolArgs {
 };
 
 // Kernel variants (bs_launch_info.kernel).
-enum KernelKind : int32_t { K_EW = 1, K_POOL_SPEC = 2, K_POOL_GENERIC = 3, K_POOL_NAIVE = 4 };
+enum KernelKind : int32_t { K_EW = 1, K_POOL_SPEC = 2, K_POOL_GENERIC = 3, K_POOL_NAIVE = 4, K_POOL_VEC = 5 };
 
 // Launchers (bs_kernels.cu).  Return the launch error (cudaSuccess on success).
 cudaError_t launch_ew(const EwArgs& a, int grid, int block, cudaStream_t st);
@@ -87,6 +87,9 @@ bool pool_has_specialisation(int kh, int kw, int sh, int sw);
 int ew_max_blocks_per_sm(int prog_class);
 // Output rows per iteration (U) of the specialised column walker for a k x k / s window.
 int pool_spec_unroll(int k, int s);
+// Vector width (4, 2) of the vector column walker for this geometry, 0 if unsupported.
+int pool_vec_width(int kh, int kw, int sh, int sw, int ph, int pw, int W, int Wo);
+int pool_vec_unroll(int vec);
 int pool_max_blocks_per_sm(int kernel_kind, const PoolArgs& a, int block);
 
 }  // namespace bs

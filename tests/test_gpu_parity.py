@@ -92,6 +92,7 @@ def test_full_size_sampled(wl, cuda_dev, oracle_lib):
 
 # ----------------------------------------------------------------------------- geometry coverage
 ODD = [1, 2, 3, 5, 7, 13, 27, 55]
+WIDTHS = [1, 2, 3, 4, 5, 7, 8, 12, 13, 14, 27, 28, 55, 56]   # even widths reach the vector walker
 
 
 @pytest.mark.parametrize("pool", [(2, 2, 0), (3, 2, 0), (3, 2, 1), (3, 1, 1), (7, 7, 0), (2, 1, 1), (5, 3, 2),
@@ -102,7 +103,7 @@ def test_odd_shapes(pool, kind, cuda_dev, oracle_lib):
     rng = random.Random(k * 100 + s * 10 + p)
     n = 0
     for H in ODD:
-        for W in ODD:
+        for W in WIDTHS:
             if H + 2 * p < k or W + 2 * p < k:
                 continue
             shape = (2, 3, H, W)
@@ -111,7 +112,7 @@ def test_odd_shapes(pool, kind, cuda_dev, oracle_lib):
             layers = [synth.batchnorm(3, 777 + H, signed_gamma=True), synth.relu() if rng.random() < .5 else synth.copy(), L]
             x = synth.uniform_np(H * 100 + W, int(np.prod(shape))).reshape(shape)
             compare(layers, x, ctx=f"{kind} k{k}s{s}p{p} {H}x{W}")
-            for g in (0, 1):
+            for g in (0, 1, 2):
                 compare(layers, x, opts={"force_generic": g, "force_rows_per_task": rng.randint(1, 5)},
                         ctx=f"{kind} k{k}s{s}p{p} {H}x{W} generic={g}")
             n += 1
@@ -129,18 +130,24 @@ def test_padding_hazard_negative_gamma(cuda_dev, oracle_lib):
 
 
 def test_tile_invariance(cuda_dev, oracle_lib):
-    """The output must not depend on the tiling: bit-identical across forced tiles."""
-    shape = (3, 5, 55, 55)
-    x = synth.uniform_np(9, int(np.prod(shape))).reshape(shape)
-    for layers in ([synth.relu(), synth.maxpool(3, 2)],
-                   [synth.batchnorm(5, 1), synth.relu(), synth.maxpool(3, 2, 1)],
-                   [synth.batchnorm(5, 2), synth.relu(), synth.avgpool(2, 2), synth.scale(0.5)]):
-        ref, _ = run_gpu(layers, x)
-        for opts in ({"force_rows_per_task": 1}, {"force_rows_per_task": 3}, {"force_rows_per_task": 7},
-                     {"force_outputs_per_group": 1}, {"force_outputs_per_group": 5},
-                     {"force_generic": 1}, {"force_generic": 1, "force_outputs_per_group": 3}):
-            got, _ = run_gpu(layers, x, opts=opts)
-            U.assert_bitexact(got, ref, f"{[L.kind for L in layers]} {opts}")
+    """The output must not depend on the tiling: bit-identical across forced tiles
+    and across the scalar / vector / runtime-geometry column walkers."""
+    for shape in [(3, 5, 55, 55), (2, 3, 56, 112)]:
+        C = shape[1]
+        x = synth.uniform_np(9, int(np.prod(shape))).reshape(shape)
+        stacks = ([synth.relu(), synth.maxpool(3, 2)],
+                  [synth.batchnorm(C, 1), synth.relu(), synth.maxpool(3, 2, 1)],
+                  [synth.batchnorm(C, 2), synth.relu(), synth.avgpool(2, 2), synth.scale(0.5)],
+                  [synth.batchnorm(C, 3, signed_gamma=True), synth.relu(), synth.maxpool(3, 2)])
+        for layers in stacks:
+            ref, _ = run_gpu(layers, x)
+            for opts in ({"force_rows_per_task": 1}, {"force_rows_per_task": 3}, {"force_rows_per_task": 7},
+                         {"force_outputs_per_group": 1}, {"force_outputs_per_group": 5},
+                         {"force_outputs_per_group": 6, "force_rows_per_task": 2},
+                         {"force_generic": 1}, {"force_generic": 2}, {"force_generic": 2, "force_rows_per_task": 5},
+                         {"force_generic": 1, "force_outputs_per_group": 3}):
+                got, _ = run_gpu(layers, x, opts=opts)
+                U.assert_bitexact(got, ref, f"{shape} {[L.kind for L in layers]} {opts}")
 
 
 @pytest.mark.parametrize("trial", range(60))
