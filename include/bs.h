@@ -99,8 +99,10 @@ typedef struct {
                                        tile (tests use it: results must not depend on tiling) */
     int32_t force_outputs_per_group;/* 0 = planner; >0 forces output columns per lane group */
     int32_t force_generic;          /* 0 = planner picks the pool kernel; 1 = force the
-                                       runtime-geometry column walker; 2 = never the vector
-                                       column walker (tests: results must not depend on it) */
+                                       runtime-geometry column walker; 2 = the global-memory
+                                       scalar walker (no vector / staged kernels); 3 = the
+                                       staged (TMA) walker where it applies, no vector walker.
+                                       Tests use it: results must not depend on the kernel */
     int32_t reserved[5];
 } bs_plan_options;
 
@@ -121,7 +123,9 @@ typedef struct {
     int32_t kernel;                 /* 1 = element-wise streaming, 2 = pool column-walker
                                        (specialised k/s), 3 = pool column-walker (runtime
                                        geometry), 4 = pool one-thread-per-output,
-                                       5 = pool vector column walker (stride 2, W % 2 == 0) */
+                                       5 = pool vector column walker (stride 2, W % 2 == 0),
+                                       6 = pool staged walker (TMA bulk copies of whole planes
+                                       into a shared-memory ring) */
     int32_t first_layer, last_layer;/* layer index range [first, last] covered */
     bs_shape in, out;
     int32_t pool_kh, pool_kw, pool_sh, pool_sw, pool_ph, pool_pw;  /* 0 if no pool */

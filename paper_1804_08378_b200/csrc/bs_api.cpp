@@ -86,6 +86,7 @@ struct Launch {
   int dst = -1;  // -1 stack output, else intermediate buffer index
   // pool geometry (kernels 2/3)
   int32_t G = 1, gw = 32, Jg = 1, n_cc = 1, rows_per_task = 1, n_rb = 1, U = 1;
+  int32_t tile_planes = 0, stages = 0;   // staged kernel
   int32_t block = 256;
   int32_t blocks_per_sm = 0;
   bool deferred = false;            // max pool: monotone prologue moved after the pool
@@ -291,6 +292,54 @@ void set_device_programs(Launch& l) {
   l.deferred = true;
 }
 
+// Staged-kernel tile: P whole planes (P*H*W*4 bytes, a multiple of 16 for the bulk copy),
+// at most kStagedTileMax bytes, preferring a task count that splits evenly over the
+// consumer warps; ring depth so that two CTAs fit one SM.  False if a plane is too big.
+constexpr int64_t kStagedTileMax = 56 * 1024;
+bool size_stages(Launch& l, int64_t n_planes, int force_rows) {
+  const int64_t HW = l.step.in.h * l.step.in.w;
+  const int p4 = HW % 4 == 0 ? 1 : (HW % 2 == 0 ? 2 : 4);
+  int step = p4;
+  while (step % l.G) step += p4;        // multiple of p4 and of G
+  int64_t pmax = kStagedTileMax / (HW * 4) / step * step;
+  const int64_t cap = (n_planes + step - 1) / step * step;
+  pmax = std::min(pmax, cap);
+  if (pmax < step) return false;
+  int64_t best = pmax;
+  for (int64_t P = pmax; P >= step; P -= step) {
+    const int64_t tasks = (P / l.G) * l.n_cc;
+    if (tasks % kStagedConsumerWarps == 0 || kStagedConsumerWarps % tasks == 0) { best = P; break; }
+  }
+  l.tile_planes = (int32_t)best;
+  const int64_t tile = best * HW * 4;
+  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, (110 * 1024) / tile));
+  l.U = pool_staged_unroll(l.step.kh, l.step.sh);
+  // split output rows so every consumer warp has a task per tile
+  const int64_t base = ((best + l.G - 1) / l.G) * l.n_cc;
+  const int64_t Ho = l.step.out.h;
+  int64_t nrb = std::min<int64_t>(Ho, (kStagedConsumerWarps + base - 1) / base);
+  if (force_rows > 0) nrb = (Ho + force_rows - 1) / force_rows;
+  l.rows_per_task = (int32_t)((Ho + nrb - 1) / nrb);
+  l.n_rb = (int32_t)((Ho + l.rows_per_task - 1) / l.rows_per_task);
+  return true;
+}
+
+// Column-walker geometry of the global-memory scalar walker (kernel 2).
+void set_spec_geometry(Launch& l, int force_opg) {
+  const Step& s = l.step;
+  l.kernel = K_POOL_SPEC;
+  int Jg = (int)std::min<int64_t>((32 - s.kw) / s.sw + 1, s.out.w);
+  if (force_opg > 0) Jg = std::min(Jg, force_opg);
+  const int ncc = (int)((s.out.w + Jg - 1) / Jg);
+  l.Jg = (int)((s.out.w + ncc - 1) / ncc);
+  l.n_cc = ncc;
+  l.gw = (l.Jg - 1) * s.sw + s.kw;
+  l.G = 32 / l.gw;
+  l.U = pool_spec_unroll(s.kh, s.sh);
+  l.rows_per_task = (int32_t)s.out.h;
+  l.n_rb = 1;
+}
+
 // ---------------------------------------------------------------- a4: sequences + tiles
 // Sequence packing: this build executes one step per sequence
 // (multi-step on-chip sequences are NEXT-2 in SURVEY §8(f)); consecutive sequences are
@@ -334,20 +383,33 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
       } else {
         l.kernel = (o.force_generic != 1 && !per_elem_max && pool_has_specialisation(s.kh, s.kw, s.sh, s.sw))
                        ? K_POOL_SPEC : K_POOL_GENERIC;
-        int jmax = (32 - s.kw) / s.sw + 1;
-        int Jg = (int)std::min<int64_t>(jmax, Wo);
-        if (o.force_outputs_per_group > 0) Jg = std::min(Jg, o.force_outputs_per_group);
-        // balance chunks: same number of chunks, as even as possible
-        const int n_cc = (int)((Wo + Jg - 1) / Jg);
-        Jg = (int)((Wo + n_cc - 1) / n_cc);
-        l.Jg = Jg;
-        l.n_cc = n_cc;
-        l.gw = (Jg - 1) * s.sw + s.kw;
-        l.G = 32 / l.gw;
-        l.U = l.kernel == K_POOL_SPEC ? pool_spec_unroll(s.kh, s.sh) : 1;
+        if (l.kernel == K_POOL_SPEC && o.force_generic != 2) {
+          // staged: one lane per output column (output-stationary), G planes per warp
+          l.kernel = K_POOL_STAGED;  // tile sized below
+          int J = (int)std::min<int64_t>(32, Wo);
+          if (o.force_outputs_per_group > 0) J = std::min(J, o.force_outputs_per_group);
+          const int ncc = (int)((Wo + J - 1) / J);
+          J = (int)((Wo + ncc - 1) / ncc);
+          l.Jg = J; l.n_cc = ncc; l.gw = J; l.G = 32 / J;
+          l.U = 1;
+        } else {
+          int jmax = (32 - s.kw) / s.sw + 1;
+          int Jg = (int)std::min<int64_t>(jmax, Wo);
+          if (o.force_outputs_per_group > 0) Jg = std::min(Jg, o.force_outputs_per_group);
+          // balance chunks: same number of chunks, as even as possible
+          const int n_cc = (int)((Wo + Jg - 1) / Jg);
+          Jg = (int)((Wo + n_cc - 1) / n_cc);
+          l.Jg = Jg;
+          l.n_cc = n_cc;
+          l.gw = (Jg - 1) * s.sw + s.kw;
+          l.G = 32 / l.gw;
+          l.U = l.kernel == K_POOL_SPEC ? pool_spec_unroll(s.kh, s.sh) : 1;
+        }
       }
       (void)Ho;
     }
+    if (l.kernel == K_POOL_STAGED && !size_stages(l, s.in.n * s.in.c, o.force_rows_per_task))
+      set_spec_geometry(l, o.force_outputs_per_group);   // plane too large to stage
     set_device_programs(l);
     if (l.kernel == K_POOL_GENERIC) l.U = 1;
     p->launches.push_back(l);
@@ -420,15 +482,20 @@ PoolArgs make_pool_args(const bs_plan* p, const Launch& l) {
   a.epi = make_prog(p, l.dev_epi, l.deferred ? (int)s.pro.size() : 0);
   a.pro_class = prog_class(l.dev_pro);
   a.epi_class = prog_class(l.dev_epi);
+  a.tile_planes = l.tile_planes;
+  a.stages = l.stages;
   return a;
 }
 
 int64_t pool_tasks(const Launch& l, int64_t n_planes) {
   if (l.kernel == K_POOL_NAIVE) return n_planes * l.step.out.h * l.step.out.w;
+  if (l.kernel == K_POOL_STAGED) return (n_planes + l.tile_planes - 1) / l.tile_planes;   // tiles
   return ((n_planes + l.G - 1) / l.G) * l.n_cc * l.n_rb;
 }
 
-int pool_grid(const Launch& l, int64_t n_tasks) {
+int pool_grid(const bs_plan* p, const Launch& l, int64_t n_tasks) {
+  if (l.kernel == K_POOL_STAGED)   // persistent: every CTA loops over tiles
+    return (int)std::max<int64_t>(1, std::min<int64_t>(n_tasks, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms));
   int64_t g = l.kernel == K_POOL_NAIVE ? (n_tasks + 255) / 256 : (n_tasks + 7) / 8;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, INT32_MAX / 2));
 }
@@ -498,7 +565,8 @@ void fill_launch_info(bs_plan* p) {
       li.rows_per_task = l.rows_per_task;
       li.halo_rows = std::max(0, s.kh - s.sh);
       li.n_tasks = pool_tasks(l, n_planes);
-      li.grid = pool_grid(l, li.n_tasks);
+      li.grid = pool_grid(p, l, li.n_tasks);
+      li.block = l.kernel == K_POOL_STAGED ? kStagedThreads : 256;
     }
     int64_t rd = s.in.numel() * 4;
     for (auto* v : {&s.pro, &s.epi})
@@ -563,8 +631,17 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       a.out = dst;
       a.plane0 = img0 * s.in.c;
       a.n_planes = (img1 - img0) * s.in.c;
-      a.n_tasks = pool_tasks(l, a.n_planes);
-      e = launch_pool(a, l.kernel, pool_grid(l, a.n_tasks), 256, st);
+      Launch lk = l;
+      if (l.kernel == K_POOL_STAGED && (a.plane0 * s.in.h * s.in.w) % 4 != 0) {
+        // sub-range not 16-B aligned for the bulk copy: global-memory walker
+        set_spec_geometry(lk, 0);
+        a.G = lk.G; a.gw = lk.gw; a.Jg = lk.Jg; a.n_cc = lk.n_cc;
+        a.rows_per_task = lk.rows_per_task; a.n_rb = lk.n_rb;
+      }
+      const int kind = lk.kernel;
+      a.n_tasks = pool_tasks(lk, a.n_planes);
+      a.n_tiles = a.n_tasks;
+      e = launch_pool(a, kind, pool_grid(p, lk, a.n_tasks), 256, st);
     }
     if (e != cudaSuccess)
       return fail(BS_ERR_CUDA, "launch %zu (layers %d..%d): %s", k, s.first_layer, s.last_layer,
@@ -699,7 +776,7 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
         bps = pool_max_blocks_per_sm(l.kernel, probe, 256);
       }
       l.blocks_per_sm = bps > 0 ? bps : 5;
-      if (l.kernel != K_POOL_NAIVE) size_rows(p, l, o, l.step.in.n * l.step.in.c);
+      if (l.kernel != K_POOL_NAIVE && l.kernel != K_POOL_STAGED) size_rows(p, l, o, l.step.in.n * l.step.in.c);
     }
   }
   fill_info(p, shapes, n_layers, n_inputs);

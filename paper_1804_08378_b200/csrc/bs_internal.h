@@ -72,11 +72,16 @@ struct PoolArgs {
   int32_t n_rb;             // row bands = ceil(Ho / rows_per_task)
   int64_t n_tasks;          // ceil(n_planes / G) * n_cc * n_rb
   int32_t pro_class, epi_class;  // ProgClass of pro / epi
+  // staged kernel (6): whole-plane tiles bulk-copied (TMA) into shared memory
+  int32_t tile_planes;      // planes per tile (tile_planes * H * W % 4 == 0)
+  int32_t stages;           // shared-memory ring depth
+  int64_t n_tiles;          // ceil(n_planes / tile_planes)
   OpProgram pro, epi;       // prologue (per input element), epilogue (per output element)
 };
 
 // Kernel variants (bs_launch_info.kernel).
-enum KernelKind : int32_t { K_EW = 1, K_POOL_SPEC = 2, K_POOL_GENERIC = 3, K_POOL_NAIVE = 4, K_POOL_VEC = 5 };
+enum KernelKind : int32_t { K_EW = 1, K_POOL_SPEC = 2, K_POOL_GENERIC = 3, K_POOL_NAIVE = 4, K_POOL_VEC = 5,
+                          K_POOL_STAGED = 6 };
 
 // Launchers (bs_kernels.cu).  Return the launch error (cudaSuccess on success).
 cudaError_t launch_ew(const EwArgs& a, int grid, int block, cudaStream_t st);
@@ -90,6 +95,11 @@ int pool_spec_unroll(int k, int s);
 // Vector width (4, 2) of the vector column walker for this geometry, 0 if unsupported.
 int pool_vec_width(int kh, int kw, int sh, int sw, int ph, int pw, int W, int Wo);
 int pool_vec_unroll(int vec);
+// Staged (TMA bulk copy + mbarrier ring) kernel: threads per CTA, and dynamic shared memory.
+constexpr int kStagedConsumerWarps = 8;
+constexpr int kStagedThreads = 32 * (kStagedConsumerWarps + 1);
+size_t pool_staged_smem(int tile_planes, int HW, int stages);
+int pool_staged_unroll(int k, int s);
 int pool_max_blocks_per_sm(int kernel_kind, const PoolArgs& a, int block);
 
 }  // namespace bs

@@ -576,6 +576,204 @@ __global__ void __launch_bounds__(kPoolBlock) pool_vec(PoolArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ staged (TMA) walker
+//
+// For planes whose rows are not 16-byte aligned (AlexNet 55/27/13, 7x7), whole-plane tiles
+// -- P contiguous planes, P*H*W*4 bytes, 16-byte aligned -- are moved HBM -> shared memory
+// by one cp.async.bulk (the 1-D TMA engine) per tile, behind an mbarrier ring of `stages`
+// buffers: warp 0 is the producer, warps 1..8 consume.  Consumers walk columns of the
+// staged planes exactly like pool_cw_spec, reading shared memory (no alignment or sector
+// waste, no halo re-reads from HBM), and store the outputs straight to HBM.  The paper's
+// stacked kernel staged patches through two smem buffers swapped per step.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+size_t pool_staged_smem(int tile_planes, int HW, int stages) {
+  const size_t tile = ((size_t)tile_planes * HW * 4 + 127) / 128 * 128;
+  return 128 + (size_t)stages * tile;   // barriers first, then the stage buffers
+}
+
+int pool_staged_unroll(int k, int s) { return k == 7 ? 1 : (s == 1 ? 4 : 4); }
+
+template <int KH, int KW, int SH, int SW, bool IS_MAX, int U, int PC, int OC>
+__global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = (uint64_t*)smem;
+  uint64_t* empty = full + 8;
+  const int HW = a.H * a.W, HWo = a.Ho * a.Wo;
+  const size_t tile_stride = ((size_t)a.tile_planes * HW * 4 + 127) / 128 * 128;
+  float* stage0 = (float*)(smem + 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (int)a.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kStagedConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer: one elected lane issues the bulk copies
+    if (lane == 0) {
+      int k = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+        const int s = k % a.stages;
+        if (k >= a.stages) mbar_wait(&empty[s], ((k / a.stages) - 1) & 1);
+        float* dst = (float*)((char*)stage0 + (size_t)s * tile_stride);
+        const int64_t pl0 = (int64_t)t * a.tile_planes;
+        const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
+        const float* src = a.in + (a.plane0 + pl0) * (int64_t)HW;
+        const uint32_t nbytes = (uint32_t)np * (uint32_t)HW * 4u;
+        const uint32_t nb16 = nbytes & ~15u;
+        for (uint32_t e = nb16 / 4; e < nbytes / 4; ++e) dst[e] = __ldg(src + e);   // <= 3 tail floats
+        if (nb16) {
+          mbar_arrive_expect_tx(&full[s], nb16);
+          bulk_g2s(dst, src, nb16, &full[s]);
+        } else {
+          mbar_arrive(&full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: output-stationary walk over the staged planes
+  // lane <-> output column j; the warp walks the output rows, each lane reducing its K
+  // window columns of every new input row straight from shared memory (row reductions
+  // of the last K-S rows slide along in registers).
+  const int cw = warp - 1;
+  const int g = lane / a.gw;
+  const int l = lane - g * a.gw;
+  const float ident = IS_MAX ? -CUDART_INF_F : 0.f;
+  const int tasks_per_tile = ((a.tile_planes + a.G - 1) / a.G) * a.n_cc * a.n_rb;
+  int k = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+    const int s = k % a.stages;
+    mbar_wait(&full[s], (k / a.stages) & 1);
+    const float* sm = (const float*)((const char*)stage0 + (size_t)s * tile_stride);
+    const int64_t pl0 = (int64_t)t * a.tile_planes;
+    const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
+    for (int task = cw; task < tasks_per_tile; task += kStagedConsumerWarps) {
+      const int rb = task % a.n_rb;
+      const int cc = (task / a.n_rb) % a.n_cc;
+      const int pg = task / (a.n_rb * a.n_cc);
+      const int pin_tile = pg * a.G + g;
+      const int j = cc * a.Jg + l;
+      const bool out_lane = (g < a.G) && (pin_tile < np) && l < a.Jg && j < a.Wo;
+      if (!out_lane) continue;   // no shuffles below: lanes are independent
+      const int64_t plane = a.plane0 + pl0 + pin_tile;
+      const int ch = (int)(plane % a.C);
+      float2 paff[kAffSlots], eaff[kAffSlots];
+      if (PC == PC_AFFINE || PC == PC_AFFINE_RELU) paff[0] = __ldg(a.pro.affine[0] + ch);
+      else if (PC == PC_GENERIC) load_affine(a.pro, ch, paff);
+      if (OC == PC_AFFINE || OC == PC_AFFINE_RELU) eaff[0] = __ldg(a.epi.affine[0] + ch);
+      else if (OC == PC_GENERIC) load_affine(a.epi, ch, eaff);
+      uint32_t flip = 0;
+      if (IS_MAX && a.epi.n_deferred > 0) {
+        if (OC == PC_AFFINE || OC == PC_AFFINE_RELU) flip = __float_as_uint(eaff[0].x) & 0x80000000u;
+        else if (OC == PC_GENERIC) flip = deferred_flip(a.epi, eaff, ch);
+      }
+      // window columns, clamped into the row: a clamped duplicate of an in-window element
+      // leaves a max unchanged (exact); for avg the out-of-range cells are zeroed below
+      const int c0 = j * SW - a.pw;
+      int coff[KW];
+      bool cval[KW];
+#pragma unroll
+      for (int v = 0; v < KW; ++v) {
+        cval[v] = (unsigned)(c0 + v) < (unsigned)a.W;
+        coff[v] = min(max(c0 + v, 0), a.W - 1);
+      }
+      const float* ps = sm + pin_tile * HW;
+      const int64_t in_idx0 = plane * (int64_t)HW;
+      float* pout = a.out + plane * (int64_t)HWo + j;
+      const int64_t out_idx0 = plane * (int64_t)HWo + j;
+
+      // reduction of input row rc (clamped; `rvalid` = the unclamped row is inside the tensor)
+      auto rowred = [&](int rc, bool rvalid) -> float {
+        const float* rp = ps + rc * a.W;
+        float acc = 0.f;
+#pragma unroll
+        for (int v = 0; v < KW; ++v) {
+          float x = rp[coff[v]];
+          if (IS_MAX) {
+            x = xorsign(x, flip);
+          } else {
+            if (PC != PC_NONE) x = apply1<PC>(a.pro, paff, ch, x, in_idx0 + (int64_t)rc * a.W + coff[v]);
+            x = (rvalid && cval[v]) ? x : 0.f;
+          }
+          acc = v == 0 ? x : red<IS_MAX>(acc, x);
+        }
+        return acc;
+      };
+
+      // blocks of B output rows: the (B-1)*S + K row reductions of a block are independent
+      constexpr int B = U;
+      constexpr int NRB = (B - 1) * SH + KH;
+      const int i0 = rb * a.rows_per_task, i1 = min(a.Ho, i0 + a.rows_per_task);
+      for (int i = i0; i < i1; i += B) {
+        const int r0 = i * SH - a.ph;
+        float h[NRB];
+        if (r0 >= 0 && r0 + NRB <= a.H) {
+#pragma unroll
+          for (int q = 0; q < NRB; ++q) h[q] = rowred(r0 + q, true);
+        } else {
+#pragma unroll
+          for (int q = 0; q < NRB; ++q) {
+            const int r = r0 + q;
+            h[q] = rowred(min(max(r, 0), a.H - 1), (unsigned)r < (unsigned)a.H);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          if (i + u < i1) {
+            float res = h[u * SH];
+#pragma unroll
+            for (int q = 1; q < KH; ++q) res = red<IS_MAX>(res, h[u * SH + q]);
+            if (IS_MAX) res = xorsign(res, flip);
+            else res = __fdiv_rn(res, a.count_include_pad ? (float)(KH * KW) : avg_div(a, i + u, j, KH, KW, SH, SW));
+            res = apply1<OC>(a.epi, eaff, ch, res, out_idx0 + (int64_t)(i + u) * a.Wo);
+            __stcs(pout + (i + u) * a.Wo, res);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
 // Column walker with runtime window geometry (any kw <= 32 - (Jg-1)*sw).
 template <bool IS_MAX>
 __global__ void __launch_bounds__(kPoolBlock) pool_cw_gen(PoolArgs a) {
@@ -720,6 +918,25 @@ int pool_vec_width(int kh, int kw, int sh, int sw, int ph, int pw, int W, int Wo
 
 int pool_vec_unroll(int vec) { return vec == 4 ? 4 : 8; }
 
+template <int K, int S, int U>
+static void* staged_pick(bool is_max, int pc, int oc) {
+  if (is_max) {
+    switch (oc) {
+      case PC_NONE: return (void*)pool_staged<K, K, S, S, true, U, PC_NONE, PC_NONE>;
+      case PC_RELU: return (void*)pool_staged<K, K, S, S, true, U, PC_NONE, PC_RELU>;
+      case PC_AFFINE_RELU: return (void*)pool_staged<K, K, S, S, true, U, PC_NONE, PC_AFFINE_RELU>;
+      default: return (void*)pool_staged<K, K, S, S, true, U, PC_NONE, PC_GENERIC>;
+    }
+  }
+  (void)oc;
+  switch (pc) {
+    case PC_NONE: return (void*)pool_staged<K, K, S, S, false, U, PC_NONE, PC_GENERIC>;
+    case PC_RELU: return (void*)pool_staged<K, K, S, S, false, U, PC_RELU, PC_GENERIC>;
+    case PC_AFFINE_RELU: return (void*)pool_staged<K, K, S, S, false, U, PC_AFFINE_RELU, PC_GENERIC>;
+    default: return (void*)pool_staged<K, K, S, S, false, U, PC_GENERIC, PC_GENERIC>;
+  }
+}
+
 static void* pool_fn(int kind, const PoolArgs& a) {
   const bool m = a.is_max != 0;
   switch (kind) {
@@ -745,6 +962,13 @@ static void* pool_fn(int kind, const PoolArgs& a) {
       }
       return nullptr;
     }
+    case K_POOL_STAGED:
+      if (m && a.pro.n > 0) return nullptr;
+      if (a.kh == 2 && a.sh == 2) return staged_pick<2, 2, 8>(m, a.pro_class, a.epi_class);
+      if (a.kh == 3 && a.sh == 2) return staged_pick<3, 2, 8>(m, a.pro_class, a.epi_class);
+      if (a.kh == 3 && a.sh == 1) return staged_pick<3, 1, 8>(m, a.pro_class, a.epi_class);
+      if (a.kh == 7 && a.sh == 7) return staged_pick<7, 7, 1>(m, a.pro_class, a.epi_class);
+      return nullptr;
     case K_POOL_GENERIC: return m ? (void*)pool_cw_gen<true> : (void*)pool_cw_gen<false>;
     case K_POOL_NAIVE: return m ? (void*)pool_naive_kernel<true> : (void*)pool_naive_kernel<false>;
     default: return nullptr;
@@ -771,6 +995,12 @@ cudaError_t launch_pool(const PoolArgs& a, int kind, int grid, int block, cudaSt
   void* fn = pool_fn(kind, a);
   if (!fn) return cudaErrorInvalidDeviceFunction;
   void* args[] = {(void*)&a};
+  if (kind == K_POOL_STAGED) {
+    const size_t smem = pool_staged_smem(a.tile_planes, a.H * a.W, a.stages);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernel(fn, dim3(grid), dim3(kStagedThreads), args, smem, st);
+  }
   return cudaLaunchKernel(fn, dim3(grid), dim3(kPoolBlock), args, 0, st);
 }
 
@@ -784,7 +1014,14 @@ int pool_max_blocks_per_sm(int kind, const PoolArgs& a, int block) {
   (void)block;
   void* fn = pool_fn(kind, a);
   int n = 0;
-  if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kPoolBlock, 0) != cudaSuccess) n = 0;
+  if (!fn) return 0;
+  if (kind == K_POOL_STAGED) {
+    const size_t smem = pool_staged_smem(a.tile_planes, a.H * a.W, a.stages);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kStagedThreads, smem) != cudaSuccess) n = 0;
+    return n;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kPoolBlock, 0) != cudaSuccess) n = 0;
   return n;
 }
 

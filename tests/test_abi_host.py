@@ -165,6 +165,9 @@ def test_tile_policy_fills_device(bs):
     halo re-reads (k - s rows per band) small."""
     for case in synth.workload("alexnet") + synth.workload("vgg16") + synth.workload("resnet50")[:1]:
         li = bs.bs_plan_query_launch(host_plan(bs, case.layers, case.shape), 0)
+        if li["kernel"] == 6:   # staged: persistent CTAs over whole-plane tiles
+            assert li["n_tasks"] >= 2 * 148 and li["block"] == 288
+            continue
         assert li["n_tasks"] >= 148 * 40
         if li["halo_rows"]:
             assert li["halo_rows"] / (li["rows_per_task"] * li["pool_sh"]) <= 1 / 8 + 1e-9
