@@ -103,7 +103,11 @@ typedef struct {
                                        scalar walker (no vector / staged kernels); 3 = the
                                        staged (TMA) walker where it applies, no vector walker.
                                        Tests use it: results must not depend on the kernel */
-    int32_t reserved[5];
+    int32_t force_tile_planes;      /* 0 = planner; >0: planes per staged (TMA) tile, rounded to
+                                       the 16-byte bulk-copy granularity */
+    int32_t force_stages;           /* 0 = planner; 2..8: shared-memory ring depth of the staged
+                                       kernel */
+    int32_t reserved[3];
 } bs_plan_options;
 
 /* Whole-plan summary. */

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _build
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("BS_LIB", _build.LIB)   # BS_LIB: an alternative build of this library
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
@@ -58,7 +58,8 @@ class bs_plan_options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("host_only", ctypes.c_int32),
                 ("max_steps_per_sequence", ctypes.c_int32), ("threads_per_block", ctypes.c_int32),
                 ("force_rows_per_task", ctypes.c_int32), ("force_outputs_per_group", ctypes.c_int32),
-                ("force_generic", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("force_generic", ctypes.c_int32), ("force_tile_planes", ctypes.c_int32),
+                ("force_stages", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class bs_plan_info(ctypes.Structure):
@@ -193,7 +194,7 @@ def bs_plan_create(layers: Sequence, input_shape, opts: Optional[dict] = None) -
         o = bs_plan_options()
         o.device = opts.get("device", -1)
         for k in ("host_only", "max_steps_per_sequence", "threads_per_block", "force_rows_per_task",
-                  "force_outputs_per_group", "force_generic"):
+                  "force_outputs_per_group", "force_generic", "force_tile_planes", "force_stages"):
             setattr(o, k, int(opts.get(k, 0)))
     h = _P()
     st = _lib.bs_plan_create(arr, len(layers), bs_shape(*[int(v) for v in input_shape]),

@@ -296,30 +296,28 @@ void set_device_programs(Launch& l) {
 // at most kStagedTileMax bytes, preferring a task count that splits evenly over the
 // consumer warps; ring depth so that two CTAs fit one SM.  False if a plane is too big.
 constexpr int64_t kStagedTileMax = 56 * 1024;
-bool size_stages(Launch& l, int64_t n_planes, int force_rows) {
+constexpr int64_t kStagedTileMin = 8 * 1024;
+bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_sms) {
   const int64_t HW = l.step.in.h * l.step.in.w;
   const int p4 = HW % 4 == 0 ? 1 : (HW % 2 == 0 ? 2 : 4);
   int step = p4;
-  while (step % l.G) step += p4;        // multiple of p4 and of G
-  int64_t pmax = kStagedTileMax / (HW * 4) / step * step;
-  const int64_t cap = (n_planes + step - 1) / step * step;
-  pmax = std::min(pmax, cap);
-  if (pmax < step) return false;
-  int64_t best = pmax;
-  for (int64_t P = pmax; P >= step; P -= step) {
-    const int64_t tasks = (P / l.G) * l.n_cc;
-    if (tasks % kStagedConsumerWarps == 0 || kStagedConsumerWarps % tasks == 0) { best = P; break; }
-  }
-  l.tile_planes = (int32_t)best;
-  const int64_t tile = best * HW * 4;
-  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, (110 * 1024) / tile));
+  while (step % l.G) step += p4;        // multiple of p4 (16-byte tiles) and of G
+  // aim for >= 8 tiles per CTA (2 CTAs per SM) so the ring runs full, within [8 KB, 56 KB]
+  const int64_t total = n_planes * HW * 4;
+  const int64_t want = std::max(kStagedTileMin, std::min(kStagedTileMax, total / (16 * (int64_t)num_sms)));
+  int64_t P = std::max<int64_t>(step, want / (HW * 4) / step * step);
+  P = std::min(P, (n_planes + step - 1) / step * step);
+  if (o.force_tile_planes > 0) P = std::max<int64_t>(step, (int64_t)o.force_tile_planes / step * step);
+  const int64_t tile = P * HW * 4;
+  if (tile > 200 * 1024) return false;   // a plane group this large is not staged
+  l.tile_planes = (int32_t)P;
+  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(8, (110 * 1024) / tile));
+  if (o.force_stages >= 2) l.stages = std::min(8, o.force_stages);
+  if ((int64_t)l.stages * tile > 220 * 1024) l.stages = (int32_t)((220 * 1024) / tile);
+  if (l.stages < 2) return false;
   l.U = pool_staged_unroll(l.step.kh, l.step.sh);
-  // split output rows so every consumer warp has a task per tile
-  const int64_t base = ((best + l.G - 1) / l.G) * l.n_cc;
   const int64_t Ho = l.step.out.h;
-  int64_t nrb = std::min<int64_t>(Ho, (kStagedConsumerWarps + base - 1) / base);
-  if (force_rows > 0) nrb = (Ho + force_rows - 1) / force_rows;
-  l.rows_per_task = (int32_t)((Ho + nrb - 1) / nrb);
+  l.rows_per_task = (int32_t)(o.force_rows_per_task > 0 ? std::min<int64_t>(Ho, o.force_rows_per_task) : Ho);
   l.n_rb = (int32_t)((Ho + l.rows_per_task - 1) / l.rows_per_task);
   return true;
 }
@@ -408,7 +406,7 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
       }
       (void)Ho;
     }
-    if (l.kernel == K_POOL_STAGED && !size_stages(l, s.in.n * s.in.c, o.force_rows_per_task))
+    if (l.kernel == K_POOL_STAGED && !size_stages(l, s.in.n * s.in.c, o, p->num_sms))
       set_spec_geometry(l, o.force_outputs_per_group);   // plane too large to stage
     set_device_programs(l);
     if (l.kernel == K_POOL_GENERIC) l.U = 1;

@@ -96,7 +96,10 @@ int pool_spec_unroll(int k, int s);
 int pool_vec_width(int kh, int kw, int sh, int sw, int ph, int pw, int W, int Wo);
 int pool_vec_unroll(int vec);
 // Staged (TMA bulk copy + mbarrier ring) kernel: threads per CTA, and dynamic shared memory.
-constexpr int kStagedConsumerWarps = 8;
+#ifndef BS_STAGED_CW
+#define BS_STAGED_CW 8
+#endif
+constexpr int kStagedConsumerWarps = BS_STAGED_CW;
 constexpr int kStagedThreads = 32 * (kStagedConsumerWarps + 1);
 size_t pool_staged_smem(int tile_planes, int HW, int stages);
 int pool_staged_unroll(int k, int s);

@@ -617,6 +617,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+#ifndef BS_BULK_CHUNK
+#define BS_BULK_CHUNK 8192
+#endif
+constexpr uint32_t kBulkChunk = BS_BULK_CHUNK;
+
 size_t pool_staged_smem(int tile_planes, int HW, int stages) {
   const size_t tile = ((size_t)tile_planes * HW * 4 + 127) / 128 * 128;
   return 128 + (size_t)stages * tile;   // barriers first, then the stage buffers
@@ -638,7 +643,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kStagedConsumerWarps);
+      mbar_init(&empty[s], ((a.tile_planes + a.G - 1) / a.G) * a.n_cc * a.n_rb);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -660,7 +665,11 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
         for (uint32_t e = nb16 / 4; e < nbytes / 4; ++e) dst[e] = __ldg(src + e);   // <= 3 tail floats
         if (nb16) {
           mbar_arrive_expect_tx(&full[s], nb16);
-          bulk_g2s(dst, src, nb16, &full[s]);
+          // several bulk copies per tile keep more requests in flight per SM
+          for (uint32_t off = 0; off < nb16; off += kBulkChunk) {
+            const uint32_t n = min(kBulkChunk, nb16 - off);
+            bulk_g2s((char*)dst + off, (const char*)src + off, n, &full[s]);
+          }
         } else {
           mbar_arrive(&full[s]);
         }
@@ -677,22 +686,32 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   const int g = lane / a.gw;
   const int l = lane - g * a.gw;
   const float ident = IS_MAX ? -CUDART_INF_F : 0.f;
+  // tasks of this CTA's tiles are dealt round-robin to the consumer warps across tiles, so
+  // a tile with fewer tasks than warps does not idle them; a stage is released when all
+  // tasks_per_tile tasks of its tile have arrived on empty[s]
   const int tasks_per_tile = ((a.tile_planes + a.G - 1) / a.G) * a.n_cc * a.n_rb;
-  int k = 0;
-  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+  const int my_tiles = (n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int my_tasks = my_tiles * tasks_per_tile;
+  for (int T = cw; T < my_tasks; T += kStagedConsumerWarps) {
+    const int k = T / tasks_per_tile;
+    const int task = T - k * tasks_per_tile;
+    const int t = (int)blockIdx.x + k * (int)gridDim.x;
     const int s = k % a.stages;
-    mbar_wait(&full[s], (k / a.stages) & 1);
-    const float* sm = (const float*)((const char*)stage0 + (size_t)s * tile_stride);
     const int64_t pl0 = (int64_t)t * a.tile_planes;
     const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
-    for (int task = cw; task < tasks_per_tile; task += kStagedConsumerWarps) {
+    const float* sm = (const float*)((const char*)stage0 + (size_t)s * tile_stride);
+    {
       const int rb = task % a.n_rb;
       const int cc = (task / a.n_rb) % a.n_cc;
       const int pg = task / (a.n_rb * a.n_cc);
       const int pin_tile = pg * a.G + g;
       const int j = cc * a.Jg + l;
       const bool out_lane = (g < a.G) && (pin_tile < np) && l < a.Jg && j < a.Wo;
-      if (!out_lane) continue;   // no shuffles below: lanes are independent
+      // every lane waits for the tile (also lanes without work: lane 0 releases the stage)
+      if (!out_lane) {
+        mbar_wait(&full[s], (k / a.stages) & 1);
+        goto task_done;
+      }
       const int64_t plane = a.plane0 + pl0 + pin_tile;
       const int ch = (int)(plane % a.C);
       float2 paff[kAffSlots], eaff[kAffSlots];
@@ -705,6 +724,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
         if (OC == PC_AFFINE || OC == PC_AFFINE_RELU) flip = __float_as_uint(eaff[0].x) & 0x80000000u;
         else if (OC == PC_GENERIC) flip = deferred_flip(a.epi, eaff, ch);
       }
+      mbar_wait(&full[s], (k / a.stages) & 1);
       // window columns, clamped into the row: a clamped duplicate of an in-window element
       // leaves a max unchanged (exact); for avg the out-of-range cells are zeroed below
       const int c0 = j * SW - a.pw;
@@ -738,37 +758,34 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
         return acc;
       };
 
-      // blocks of B output rows: the (B-1)*S + K row reductions of a block are independent
-      constexpr int B = U;
-      constexpr int NRB = (B - 1) * SH + KH;
+      // rolling window over output rows: each output row reduces its S new input rows (all
+      // K rows when K <= S) and the K - S rows carried from the previous output row
+      constexpr int CARRY = KH > SH ? KH - SH : 0;
+      constexpr int NEW = KH - CARRY;
       const int i0 = rb * a.rows_per_task, i1 = min(a.Ho, i0 + a.rows_per_task);
-      for (int i = i0; i < i1; i += B) {
+      auto rowred_any = [&](int r) -> float {
+        return rowred(min(max(r, 0), a.H - 1), (unsigned)r < (unsigned)a.H);
+      };
+      float hist[KH > 1 ? KH : 1];
+#pragma unroll
+      for (int u = 0; u < CARRY; ++u) hist[u] = rowred_any(i0 * SH - a.ph + u);
+#pragma unroll 4
+      for (int i = i0; i < i1; ++i) {
         const int r0 = i * SH - a.ph;
-        float h[NRB];
-        if (r0 >= 0 && r0 + NRB <= a.H) {
 #pragma unroll
-          for (int q = 0; q < NRB; ++q) h[q] = rowred(r0 + q, true);
-        } else {
+        for (int u = 0; u < NEW; ++u) hist[CARRY + u] = rowred_any(r0 + CARRY + u);
+        float res = hist[0];
 #pragma unroll
-          for (int q = 0; q < NRB; ++q) {
-            const int r = r0 + q;
-            h[q] = rowred(min(max(r, 0), a.H - 1), (unsigned)r < (unsigned)a.H);
-          }
-        }
+        for (int q = 1; q < KH; ++q) res = red<IS_MAX>(res, hist[q]);
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-          if (i + u < i1) {
-            float res = h[u * SH];
-#pragma unroll
-            for (int q = 1; q < KH; ++q) res = red<IS_MAX>(res, h[u * SH + q]);
-            if (IS_MAX) res = xorsign(res, flip);
-            else res = __fdiv_rn(res, a.count_include_pad ? (float)(KH * KW) : avg_div(a, i + u, j, KH, KW, SH, SW));
-            res = apply1<OC>(a.epi, eaff, ch, res, out_idx0 + (int64_t)(i + u) * a.Wo);
-            __stcs(pout + (i + u) * a.Wo, res);
-          }
-        }
+        for (int u = 0; u < CARRY; ++u) hist[u] = hist[u + NEW];
+        if (IS_MAX) res = xorsign(res, flip);
+        else res = __fdiv_rn(res, a.count_include_pad ? (float)(KH * KW) : avg_div(a, i, j, KH, KW, SH, SW));
+        res = apply1<OC>(a.epi, eaff, ch, res, out_idx0 + (int64_t)i * a.Wo);
+        __stcs(pout + i * a.Wo, res);
       }
     }
+  task_done:
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
