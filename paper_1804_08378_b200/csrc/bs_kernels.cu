@@ -305,6 +305,14 @@ __device__ __forceinline__ float avg_div(const PoolArgs& a, int i, int j, int kh
 
 constexpr int kPoolBlock = 256;
 
+// x / D for a compile-time divisor: an exact power-of-two scaling when D is a power of two
+// (x * 2^-k is the correctly rounded x / 2^k), IEEE division otherwise.
+template <int D>
+__device__ __forceinline__ float div_by(float x) {
+  if ((D & (D - 1)) == 0) return __fmul_rn(x, 1.0f / (float)D);
+  return __fdiv_rn(x, (float)D);
+}
+
 // Per-task lane geometry shared by both column walkers.
 struct LaneTask {
   int64_t plane;
@@ -399,7 +407,7 @@ __global__ void __launch_bounds__(kPoolBlock) pool_cw_spec(PoolArgs a) {
 #pragma unroll
           for (int d = 1; d < KW; ++d) res = red<IS_MAX>(res, __shfl_down_sync(0xffffffffu, acc, d));
           if (IS_MAX) res = xorsign(res, flip);
-          else res = __fdiv_rn(res, a.count_include_pad ? (float)(KH * KW) : avg_div(a, i + u, T.j, KH, KW, SH, SW));
+          else res = a.count_include_pad ? div_by<KH * KW>(res) : __fdiv_rn(res, avg_div(a, i + u, T.j, KH, KW, SH, SW));
           res = apply1<OC>(a.epi, eaff, ch, res, out_idx0 + (int64_t)(i + u) * a.Wo);
           if (T.out_lane) __stcs((float*)(po + (size_t)u * Wo4), res);
         }
@@ -449,7 +457,7 @@ __global__ void __launch_bounds__(kPoolBlock) pool_cw_spec(PoolArgs a) {
 // neighbour lane (__shfl_up for pad 1, __shfl_down for pad 0).  That neighbour is a "halo
 // lane" at the group's edge which loads but produces nothing.  Requires no right padding.
 template <int K, int PADL, int VEC, bool IS_MAX, int U, int PC, int OC>
-__global__ void __launch_bounds__(kPoolBlock) pool_vec(PoolArgs a) {
+__global__ void __launch_bounds__(kPoolBlock, 4) pool_vec(PoolArgs a) {
   constexpr int S = 2, OPL = VEC / 2;
   constexpr int NR = (U - 1) * S + K;
   constexpr int HL = (K == 3 && PADL == 1) ? 1 : 0;   // left halo lane
@@ -558,7 +566,7 @@ __global__ void __launch_bounds__(kPoolBlock) pool_vec(PoolArgs a) {
           for (int t2_ = 0; t2_ < OPL; ++t2_) {
             float r = o[t2_];
             if (IS_MAX) r = xorsign(r, flip);
-            else r = __fdiv_rn(r, a.count_include_pad ? (float)(K * K) : avg_div(a, iu, j + t2_, K, K, S, S));
+            else r = a.count_include_pad ? div_by<K * K>(r) : __fdiv_rn(r, avg_div(a, iu, j + t2_, K, K, S, S));
             o[t2_] = apply1<OC>(a.epi, eaff, ch, r, out_idx0 + (int64_t)iu * a.Wo + t2_);
           }
           if (out_lane) {
@@ -780,7 +788,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
 #pragma unroll
         for (int u = 0; u < CARRY; ++u) hist[u] = hist[u + NEW];
         if (IS_MAX) res = xorsign(res, flip);
-        else res = __fdiv_rn(res, a.count_include_pad ? (float)(KH * KW) : avg_div(a, i, j, KH, KW, SH, SW));
+        else res = a.count_include_pad ? div_by<KH * KW>(res) : __fdiv_rn(res, avg_div(a, i, j, KH, KW, SH, SW));
         res = apply1<OC>(a.epi, eaff, ch, res, out_idx0 + (int64_t)i * a.Wo);
         __stcs(pout + i * a.Wo, res);
       }
