@@ -181,6 +181,7 @@ def main():
     ap.add_argument("--out", default="", help="also append the JSON line to this file")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of CUDA graph replays")
     ap.add_argument("--per-stack", action="store_true", help="add a per-stack timing breakdown")
+    ap.add_argument("--strong", action="store_true", help="split the BASELINE batch over ranks (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -190,16 +191,29 @@ def main():
     import torch.distributed as dist
 
     import paper_1804_08378_b200 as bs
+    from paper_1804_08378_b200 import dist as bsd
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; BS_BENCH_BACKEND=gloo lets several ranks share one GPU (testing the
+    # multi-rank path on a 1-GPU box)
+    backend = os.environ.get("BS_BENCH_BACKEND", "nccl")
+    local_dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
-    batch = args.batch or synth.DEFAULT_BATCH[args.workload]
+    full_batch = args.batch or synth.DEFAULT_BATCH[args.workload]
+    if args.strong:   # strong scaling: the BASELINE batch is split over the ranks
+        lo, hi = bsd.shard(full_batch, world, rank)
+        batch = hi - lo
+    else:             # weak scaling: every rank runs the BASELINE batch
+        batch = full_batch
     cases = synth.workload(args.workload, batch=batch)
     inst = instances(cases)
     plans = {}
@@ -311,20 +325,14 @@ def main():
     last = bufs[(args.warmup + args.steps - 1) % n_sets]
     csum = float(sum(y.double().sum().item() for _, y in last))
     finite = all(bool(torch.isfinite(y).all()) for _, y in last)
-    if world > 1:
-        t = torch.tensor([ms, dom_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, dom_ms = float(t[0]), float(t[1])
-        cs = torch.tensor([csum, float(finite)], device=dev, dtype=torch.float64)
-        gathered = [torch.zeros_like(cs) for _ in range(world)]
-        dist.all_gather(gathered, cs)
-        checksums = [float(g[0]) for g in gathered]
-        finite = all(bool(g[1]) for g in gathered)
-    else:
-        checksums = [csum]
+    # max over ranks of the device times; per-rank checksums (outside the timed region)
+    ms, dom_ms = bsd.max_over_ranks([ms, dom_ms], dev)
+    gathered = bsd.gather_stats([csum, float(finite), float(batch)], dev)
+    checksums = [g[0] for g in gathered]
+    finite = all(bool(g[1]) for g in gathered)
+    images = int(sum(g[2] for g in gathered))
 
     ms_step = ms / args.steps
-    images = batch * world
     ips = images / (ms_step / 1e3)
     gbs_rank = step_bytes / (ms_step / 1e3) / 1e9
     peak, peak_src = load_peaks()
@@ -395,10 +403,7 @@ def main():
     b.record(stream)
     torch.cuda.synchronize()
     e2e_ms = a.elapsed_time(b)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t[0])
+    e2e_ms = bsd.max_over_ranks([e2e_ms], dev)[0]
     e2e = {"value": images / (e2e_ms / e2e_steps / 1e3), "unit": "images/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
            "path": "bs_execute_host: pinned host -> device copy, kernels, device -> host copy, pipelined per chunk"}
@@ -464,10 +469,11 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 seeded NCHW fp32, BN params per SURVEY §8(d))",
             "config": {"workload": args.workload, "baseline_config_index": CONFIG_INDEX[args.workload],
                        "global_batch": images, "per_gpu_batch": batch, "stacks_per_step": len(inst),
+                       "backend": backend if world > 1 else None,
                        "parallelism": f"batch-sharded dp{world} (independent images, no data-path collective)",
                        "launch": "CUDA graph replay per step" if graphs else "eager launches",
                        "l2": (f"rotating {n_sets} buffer sets ({n_sets * step_bytes / 1e9:.2f} GB > 4x L2 "
