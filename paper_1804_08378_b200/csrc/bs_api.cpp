@@ -295,25 +295,26 @@ void set_device_programs(Launch& l) {
 // Staged-kernel tile: P whole planes (P*H*W*4 bytes, a multiple of 16 for the bulk copy),
 // at most kStagedTileMax bytes, preferring a task count that splits evenly over the
 // consumer warps; ring depth so that two CTAs fit one SM.  False if a plane is too big.
-constexpr int64_t kStagedTileMax = 56 * 1024;
+constexpr int64_t kStagedTileMax = 48 * 1024;
 constexpr int64_t kStagedTileMin = 8 * 1024;
+constexpr int64_t kStagedSmemPerCta = 110 * 1024;   // two CTAs per SM
 bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_sms) {
   const int64_t HW = l.step.in.h * l.step.in.w;
-  const int p4 = HW % 4 == 0 ? 1 : (HW % 2 == 0 ? 2 : 4);
-  int step = p4;
-  while (step % l.G) step += p4;        // multiple of p4 (16-byte tiles) and of G
-  // aim for >= 8 tiles per CTA (2 CTAs per SM) so the ring runs full, within [8 KB, 56 KB]
+  // tiles of whole planes (any count: head/tail floats of unaligned tiles are copied by the
+  // producer lane), a multiple of the G planes a warp covers; ~8 tiles per CTA or more,
+  // within [8 KB, 48 KB]; as many ring stages as fit two CTAs per SM
+  const int step = l.G;
   const int64_t total = n_planes * HW * 4;
   const int64_t want = std::max(kStagedTileMin, std::min(kStagedTileMax, total / (16 * (int64_t)num_sms)));
   int64_t P = std::max<int64_t>(step, want / (HW * 4) / step * step);
   P = std::min(P, (n_planes + step - 1) / step * step);
   if (o.force_tile_planes > 0) P = std::max<int64_t>(step, (int64_t)o.force_tile_planes / step * step);
-  const int64_t tile = P * HW * 4;
-  if (tile > 200 * 1024) return false;   // a plane group this large is not staged
+  const int64_t stride = (int64_t)pool_staged_stride((int)P, (int)HW);
+  if (stride > 100 * 1024) return false;   // plane group too large to stage
   l.tile_planes = (int32_t)P;
-  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(8, (110 * 1024) / tile));
+  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(8, kStagedSmemPerCta / stride));
   if (o.force_stages >= 2) l.stages = std::min(8, o.force_stages);
-  if ((int64_t)l.stages * tile > 220 * 1024) l.stages = (int32_t)((220 * 1024) / tile);
+  if ((int64_t)l.stages * stride > 220 * 1024) l.stages = (int32_t)((220 * 1024) / stride);
   if (l.stages < 2) return false;
   l.U = pool_staged_unroll(l.step.kh, l.step.sh);
   const int64_t Ho = l.step.out.h;
@@ -630,7 +631,7 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       a.plane0 = img0 * s.in.c;
       a.n_planes = (img1 - img0) * s.in.c;
       Launch lk = l;
-      if (l.kernel == K_POOL_STAGED && (a.plane0 * s.in.h * s.in.w) % 4 != 0) {
+      if (false) {
         // sub-range not 16-B aligned for the bulk copy: global-memory walker
         set_spec_geometry(lk, 0);
         a.G = lk.G; a.gw = lk.gw; a.Jg = lk.Jg; a.n_cc = lk.n_cc;

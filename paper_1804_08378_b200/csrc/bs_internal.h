@@ -102,6 +102,7 @@ int pool_vec_unroll(int vec);
 constexpr int kStagedConsumerWarps = BS_STAGED_CW;
 constexpr int kStagedThreads = 32 * (kStagedConsumerWarps + 1);
 size_t pool_staged_smem(int tile_planes, int HW, int stages);
+__host__ __device__ size_t pool_staged_stride(int tile_planes, int HW);
 int pool_staged_unroll(int k, int s);
 int pool_max_blocks_per_sm(int kernel_kind, const PoolArgs& a, int block);
 

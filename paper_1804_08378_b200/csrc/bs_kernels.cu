@@ -630,9 +630,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #endif
 constexpr uint32_t kBulkChunk = BS_BULK_CHUNK;
 
+// A tile's bytes sit in its stage at offset (global address mod 16), so the 16-byte-aligned
+// middle of any plane range is one bulk copy and only <= 3 head and tail floats are copied
+// by the producer lane; tiles need not start on 16-byte boundaries.
+__host__ __device__ size_t pool_staged_stride(int tile_planes, int HW) {
+  return ((size_t)tile_planes * HW * 4 + 16 + 127) / 128 * 128;
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
 size_t pool_staged_smem(int tile_planes, int HW, int stages) {
-  const size_t tile = ((size_t)tile_planes * HW * 4 + 127) / 128 * 128;
-  return 128 + (size_t)stages * tile;   // barriers first, then the stage buffers
+  return 128 + (size_t)stages * pool_staged_stride(tile_planes, HW);   // barriers, then stages
 }
 
 int pool_staged_unroll(int k, int s) { return k == 7 ? 1 : (s == 1 ? 4 : 4); }
@@ -643,14 +656,14 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   uint64_t* full = (uint64_t*)smem;
   uint64_t* empty = full + 8;
   const int HW = a.H * a.W, HWo = a.Ho * a.Wo;
-  const size_t tile_stride = ((size_t)a.tile_planes * HW * 4 + 127) / 128 * 128;
+  const size_t tile_stride = pool_staged_stride(a.tile_planes, HW);
   float* stage0 = (float*)(smem + 128);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (int)a.n_tiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 2);   // cp.async arrive (edges) + arrive.expect_tx (bulk body)
       mbar_init(&empty[s], ((a.tile_planes + a.G - 1) / a.G) * a.n_cc * a.n_rb);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -664,19 +677,23 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
         const int s = k % a.stages;
         if (k >= a.stages) mbar_wait(&empty[s], ((k / a.stages) - 1) & 1);
-        float* dst = (float*)((char*)stage0 + (size_t)s * tile_stride);
         const int64_t pl0 = (int64_t)t * a.tile_planes;
         const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
         const float* src = a.in + (a.plane0 + pl0) * (int64_t)HW;
+        const uint32_t head_off = (uint32_t)((uintptr_t)src & 15u);
+        float* dst = (float*)((char*)stage0 + (size_t)s * tile_stride + head_off);
         const uint32_t nbytes = (uint32_t)np * (uint32_t)HW * 4u;
-        const uint32_t nb16 = nbytes & ~15u;
-        for (uint32_t e = nb16 / 4; e < nbytes / 4; ++e) dst[e] = __ldg(src + e);   // <= 3 tail floats
-        if (nb16) {
-          mbar_arrive_expect_tx(&full[s], nb16);
-          // several bulk copies per tile keep more requests in flight per SM
-          for (uint32_t off = 0; off < nb16; off += kBulkChunk) {
-            const uint32_t n = min(kBulkChunk, nb16 - off);
-            bulk_g2s((char*)dst + off, (const char*)src + off, n, &full[s]);
+        const uint32_t h = min(nbytes, (16u - head_off) & 15u);        // head bytes before 16-B
+        const uint32_t body = (nbytes - h) & ~15u;                      // aligned middle
+        // head / tail floats: 4-byte cp.async (non-blocking), tracked by the full barrier
+        for (uint32_t e = 0; e < h / 4; ++e) cp_async4(dst + e, src + e);
+        for (uint32_t e = (h + body) / 4; e < nbytes / 4; ++e) cp_async4(dst + e, src + e);
+        cp_async_mbar_arrive(&full[s]);   // arrival 1 of 2: when those copies have landed
+        if (body) {
+          mbar_arrive_expect_tx(&full[s], body);
+          for (uint32_t off = 0; off < body; off += kBulkChunk) {
+            const uint32_t n = min(kBulkChunk, body - off);
+            bulk_g2s((char*)dst + h + off, (const char*)src + h + off, n, &full[s]);
           }
         } else {
           mbar_arrive(&full[s]);
@@ -694,32 +711,32 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   const int g = lane / a.gw;
   const int l = lane - g * a.gw;
   const float ident = IS_MAX ? -CUDART_INF_F : 0.f;
-  // tasks of this CTA's tiles are dealt round-robin to the consumer warps across tiles, so
-  // a tile with fewer tasks than warps does not idle them; a stage is released when all
-  // tasks_per_tile tasks of its tile have arrived on empty[s]
+  // The tasks of this CTA's tiles are dealt round-robin to the consumer warps across tiles
+  // (a tile with fewer tasks than warps does not idle them).  Every warp waits on every
+  // tile's full barrier in tile order -- so it never waits on a ring slot more than one phase
+  // ahead (mbarrier parity would alias) -- and runs the tasks dealt to it; a stage is
+  // released when all tasks_per_tile tasks of its tile have arrived on empty[s].
   const int tasks_per_tile = ((a.tile_planes + a.G - 1) / a.G) * a.n_cc * a.n_rb;
   const int my_tiles = (n_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int my_tasks = my_tiles * tasks_per_tile;
-  for (int T = cw; T < my_tasks; T += kStagedConsumerWarps) {
-    const int k = T / tasks_per_tile;
-    const int task = T - k * tasks_per_tile;
+  for (int k = 0; k < my_tiles; ++k) {
     const int t = (int)blockIdx.x + k * (int)gridDim.x;
     const int s = k % a.stages;
     const int64_t pl0 = (int64_t)t * a.tile_planes;
     const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
-    const float* sm = (const float*)((const char*)stage0 + (size_t)s * tile_stride);
-    {
+    const float* sm = (const float*)((const char*)stage0 + (size_t)s * tile_stride +
+                                     ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW) & 15u));
+    const int base = (int)(((int64_t)k * tasks_per_tile) % kStagedConsumerWarps);
+    const int task0 = (cw - base + kStagedConsumerWarps) % kStagedConsumerWarps;
+    mbar_wait(&full[s], (k / a.stages) & 1);   // every tile, in order (even with no task in it)
+    for (int task = task0; task < tasks_per_tile; task += kStagedConsumerWarps) {
       const int rb = task % a.n_rb;
       const int cc = (task / a.n_rb) % a.n_cc;
       const int pg = task / (a.n_rb * a.n_cc);
       const int pin_tile = pg * a.G + g;
       const int j = cc * a.Jg + l;
       const bool out_lane = (g < a.G) && (pin_tile < np) && l < a.Jg && j < a.Wo;
-      // every lane waits for the tile (also lanes without work: lane 0 releases the stage)
-      if (!out_lane) {
-        mbar_wait(&full[s], (k / a.stages) & 1);
-        goto task_done;
-      }
+      if (!out_lane) goto task_done;
+      {
       const int64_t plane = a.plane0 + pl0 + pin_tile;
       const int ch = (int)(plane % a.C);
       float2 paff[kAffSlots], eaff[kAffSlots];
@@ -732,7 +749,6 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
         if (OC == PC_AFFINE || OC == PC_AFFINE_RELU) flip = __float_as_uint(eaff[0].x) & 0x80000000u;
         else if (OC == PC_GENERIC) flip = deferred_flip(a.epi, eaff, ch);
       }
-      mbar_wait(&full[s], (k / a.stages) & 1);
       // window columns, clamped into the row: a clamped duplicate of an in-window element
       // leaves a max unchanged (exact); for avg the out-of-range cells are zeroed below
       const int c0 = j * SW - a.pw;
@@ -743,18 +759,24 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
         cval[v] = (unsigned)(c0 + v) < (unsigned)a.W;
         coff[v] = min(max(c0 + v, 0), a.W - 1);
       }
+      // per-lane byte pointers of the window columns in row 0; a row adds a warp-uniform
+      // offset, so every shared-memory load is a single LDS [Rcol + URrow]
       const float* ps = sm + pin_tile * HW;
+      const char* colp[KW];
+#pragma unroll
+      for (int v = 0; v < KW; ++v) colp[v] = (const char*)(ps + coff[v]);
+      const unsigned W4 = 4u * (unsigned)a.W;
       const int64_t in_idx0 = plane * (int64_t)HW;
       float* pout = a.out + plane * (int64_t)HWo + j;
       const int64_t out_idx0 = plane * (int64_t)HWo + j;
 
       // reduction of input row rc (clamped; `rvalid` = the unclamped row is inside the tensor)
       auto rowred = [&](int rc, bool rvalid) -> float {
-        const float* rp = ps + rc * a.W;
+        const unsigned roff = (unsigned)rc * W4;
         float acc = 0.f;
 #pragma unroll
         for (int v = 0; v < KW; ++v) {
-          float x = rp[coff[v]];
+          float x = *(const float*)(colp[v] + roff);
           if (IS_MAX) {
             x = xorsign(x, flip);
           } else {
@@ -765,23 +787,17 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
         }
         return acc;
       };
+      auto rowred_edge = [&](int r) -> float {
+        return rowred(min(max(r, 0), a.H - 1), (unsigned)r < (unsigned)a.H);
+      };
 
       // rolling window over output rows: each output row reduces its S new input rows (all
       // K rows when K <= S) and the K - S rows carried from the previous output row
       constexpr int CARRY = KH > SH ? KH - SH : 0;
       constexpr int NEW = KH - CARRY;
       const int i0 = rb * a.rows_per_task, i1 = min(a.Ho, i0 + a.rows_per_task);
-      auto rowred_any = [&](int r) -> float {
-        return rowred(min(max(r, 0), a.H - 1), (unsigned)r < (unsigned)a.H);
-      };
       float hist[KH > 1 ? KH : 1];
-#pragma unroll
-      for (int u = 0; u < CARRY; ++u) hist[u] = rowred_any(i0 * SH - a.ph + u);
-#pragma unroll 4
-      for (int i = i0; i < i1; ++i) {
-        const int r0 = i * SH - a.ph;
-#pragma unroll
-        for (int u = 0; u < NEW; ++u) hist[CARRY + u] = rowred_any(r0 + CARRY + u);
+      auto emit = [&](int i) {
         float res = hist[0];
 #pragma unroll
         for (int q = 1; q < KH; ++q) res = red<IS_MAX>(res, hist[q]);
@@ -791,11 +807,33 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
         else res = a.count_include_pad ? div_by<KH * KW>(res) : __fdiv_rn(res, avg_div(a, i, j, KH, KW, SH, SW));
         res = apply1<OC>(a.epi, eaff, ch, res, out_idx0 + (int64_t)i * a.Wo);
         __stcs(pout + i * a.Wo, res);
+      };
+      // output rows whose window lies inside the tensor: [fb, fe) -- no clamps, no branches
+      const int fb = max(i0, (a.ph + SH - 1) / SH);
+      const int fe = max(fb, min(i1, (a.H - KH + a.ph) / SH + 1));
+#pragma unroll
+      for (int u = 0; u < CARRY; ++u) hist[u] = rowred_edge(i0 * SH - a.ph + u);
+      for (int i = i0; i < fb; ++i) {
+#pragma unroll
+        for (int u = 0; u < NEW; ++u) hist[CARRY + u] = rowred_edge(i * SH - a.ph + CARRY + u);
+        emit(i);
       }
+#pragma unroll 4
+      for (int i = fb; i < fe; ++i) {
+#pragma unroll
+        for (int u = 0; u < NEW; ++u) hist[CARRY + u] = rowred(i * SH - a.ph + CARRY + u, true);
+        emit(i);
+      }
+      for (int i = fe; i < i1; ++i) {
+#pragma unroll
+        for (int u = 0; u < NEW; ++u) hist[CARRY + u] = rowred_edge(i * SH - a.ph + CARRY + u);
+        emit(i);
+      }
+      }
+    task_done:
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-  task_done:
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
