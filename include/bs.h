@@ -91,9 +91,9 @@ typedef struct {
     int32_t device;                 /* CUDA device ordinal; -1 = current device */
     int32_t host_only;              /* 1 = plan on the host only (no device memory; the plan can
                                        be queried but not executed); used by CPU tests */
-    int32_t max_steps_per_sequence; /* 0 = unlimited; 1 and 5 mirror the paper's policies
-                                       (P:L677-678).  This build executes one step per sequence
-                                       (see DESIGN.md), so values other than 1 are clamped. */
+    int32_t max_steps_per_sequence; /* 0 = unlimited (up to 16 steps and what fits on chip);
+                                       1 and 5 mirror the paper's policies.  A
+                                       sequence of >= 2 steps runs on-chip in one launch */
     int32_t threads_per_block;      /* 0 = planner default (multiple of 32, <= 1024) */
     int32_t force_rows_per_task;    /* 0 = planner; >0 forces the output-row band of a pool
                                        tile (tests use it: results must not depend on tiling) */
@@ -122,14 +122,16 @@ typedef struct {
     int64_t intermediate_bytes;     /* plan-owned buffers between serialised sequences */
 } bs_plan_info;
 
-/* Per-launch (= per sequence) details. */
+/* Per-launch (= per sequence) details.  For kernel 7, groups_per_warp = steps fused and
+ * outputs_per_group = planes per staged tile. */
 typedef struct {
     int32_t kernel;                 /* 1 = element-wise streaming, 2 = pool column-walker
                                        (specialised k/s), 3 = pool column-walker (runtime
                                        geometry), 4 = pool one-thread-per-output,
                                        5 = pool vector column walker (stride 2, W % 2 == 0),
                                        6 = pool staged walker (TMA bulk copies of whole planes
-                                       into a shared-memory ring) */
+                                       into a shared-memory ring), 7 = on-chip multi-step
+                                       sequence (same staging; steps ping-pong in smem) */
     int32_t first_layer, last_layer;/* layer index range [first, last] covered */
     bs_shape in, out;
     int32_t pool_kh, pool_kw, pool_sh, pool_sw, pool_ph, pool_pw;  /* 0 if no pool */

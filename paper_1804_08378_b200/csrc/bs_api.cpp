@@ -90,6 +90,9 @@ struct Launch {
   int32_t block = 256;
   int32_t blocks_per_sm = 0;
   bool deferred = false;            // max pool: monotone prologue moved after the pool
+  std::vector<Step> seq;            // K_SEQ: the steps of the on-chip sequence
+  size_t seq_off = 0;               // K_SEQ: index of its first descriptor in the plan's array
+  int32_t seq_work_floats = 0;      // K_SEQ: floats per shared-memory work buffer
   std::vector<HostOp> dev_pro, dev_epi;  // programs as the kernel runs them
   bs_launch_info info{};
 };
@@ -102,7 +105,9 @@ struct bs_plan {
   int num_sms = 148;
   bs_plan_info info{};
   std::vector<Launch> launches;
+  std::vector<Step> steps;             // every step of the stack, in order
   float2* params = nullptr;            // device parameter block
+  SeqStepDev* seq_steps = nullptr;     // device descriptors of on-chip sequences
   float* inter[2] = {nullptr, nullptr};  // intermediates between serialised sequences
   cudaStream_t copy_stream[2] = {nullptr, nullptr};  // bs_execute_host pipelines
   cudaEvent_t ev_pool[64] = {};
@@ -348,15 +353,8 @@ void set_spec_geometry(Launch& l, int force_opg) {
 //                       rows_per_task output rows.  The on-chip footprint of a task is the
 //                       ((U-1)*s + k) x gw register window per warp -- the B200 analogue of
 //                       the paper's "data per step x SIMD units".
-void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& o) {
-  p->launches.clear();
-  int inter_idx = 0;
-  for (size_t k = 0; k < steps.size(); ++k) {
-    Launch l;
-    l.step = steps[k];
-    l.src = k == 0 ? -1 : (int)((inter_idx + 1) % 2);
-    l.dst = k + 1 == steps.size() ? -1 : inter_idx;
-    if (k + 1 < steps.size()) inter_idx = (inter_idx + 1) % 2;
+// Kernel and tile geometry of a single-step launch.
+void configure_step_launch(bs_plan* p, Launch& l, const bs_plan_options& o) {
     const Step& s = l.step;
     if (!s.has_pool) {
       l.kernel = K_EW;
@@ -411,6 +409,80 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
       set_spec_geometry(l, o.force_outputs_per_group);   // plane too large to stage
     set_device_programs(l);
     if (l.kernel == K_POOL_GENERIC) l.U = 1;
+}
+
+bool has_add(const Step& s) {
+  for (auto* v : {&s.pro, &s.epi})
+    for (const HostOp& op : *v)
+      if (op.kind == DOP_ADD) return true;
+  return false;
+}
+
+// Shared memory of an on-chip sequence over steps [a, b) at P planes per tile, 2 stages.
+int64_t seq_bytes(const std::vector<Step>& st, size_t a, size_t b, int64_t P, int stages, int64_t* work_floats) {
+  const int64_t HW0 = st[a].in.h * st[a].in.w;
+  int64_t inter = 1;
+  for (size_t k = a; k + 1 < b; ++k) inter = std::max<int64_t>(inter, st[k].out.h * st[k].out.w);
+  if (work_floats) *work_floats = P * inter;
+  return 128 + stages * (int64_t)pool_staged_stride((int)P, (int)HW0) + 2 * P * inter * 4 + 256;
+}
+
+// a4 sequence packing (lst:collapse #4): greedily add the next step while the
+// sequence still fits on chip -- here: whole planes of the first input and of every
+// intermediate in shared memory (no halos) -- and the policy's step limit allows it.
+// A step with an ADD operand (per-execute pointers) is kept in a sequence of its own.
+bool seq_fits(const std::vector<Step>& st, size_t a, size_t b) {
+  for (size_t k = a; k < b; ++k)
+    if (has_add(st[k])) return false;
+  return seq_bytes(st, a, b, 1, 2, nullptr) <= 220 * 1024;
+}
+
+void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& o) {
+  p->launches.clear();
+  size_t max_steps = o.max_steps_per_sequence <= 0 ? (size_t)kMaxSeqSteps
+                                                   : std::min<size_t>(kMaxSeqSteps, o.max_steps_per_sequence);
+  std::vector<std::pair<size_t, size_t>> seqs;
+  for (size_t a = 0; a < steps.size();) {
+    size_t b = a + 1;
+    while (b < steps.size() && b - a < max_steps && seq_fits(steps, a, b + 1)) ++b;
+    seqs.emplace_back(a, b);
+    a = b;
+  }
+  int inter_idx = 0;
+  for (size_t k = 0; k < seqs.size(); ++k) {
+    const size_t a = seqs[k].first, b = seqs[k].second;
+    Launch l;
+    l.src = k == 0 ? -1 : (int)((inter_idx + 1) % 2);
+    l.dst = k + 1 == seqs.size() ? -1 : inter_idx;
+    if (k + 1 < seqs.size()) inter_idx = (inter_idx + 1) % 2;
+    if (b - a == 1) {
+      l.step = steps[a];
+      configure_step_launch(p, l, o);
+    } else {
+      l.kernel = K_SEQ;
+      l.seq.assign(steps.begin() + a, steps.begin() + b);
+      l.step = Step();
+      l.step.first_layer = steps[a].first_layer;
+      l.step.last_layer = steps[b - 1].last_layer;
+      l.step.in = steps[a].in;
+      l.step.out = steps[b - 1].out;
+      l.step.has_pool = true;
+      l.step.kh = steps[a].kh; l.step.kw = steps[a].kw; l.step.sh = steps[a].sh;
+      l.step.sw = steps[a].sw; l.step.ph = steps[a].ph; l.step.pw = steps[a].pw;
+      // planes per tile: the most that keep two CTAs per SM (else one), >= 8 tiles per CTA
+      const int64_t n_planes = steps[a].in.n * steps[a].in.c;
+      int64_t P = 1;
+      while (P * 2 <= n_planes / (8 * 2 * p->num_sms) && seq_bytes(steps, a, b, P * 2, 2, nullptr) <= 110 * 1024) P *= 2;
+      if (o.force_tile_planes > 0) P = o.force_tile_planes;
+      int stages = 2;
+      while (stages < 4 && seq_bytes(steps, a, b, P, stages + 1, nullptr) <= 110 * 1024) ++stages;
+      if (seq_bytes(steps, a, b, P, stages, nullptr) > 220 * 1024) { P = 1; stages = 2; }
+      int64_t wf = 0;
+      seq_bytes(steps, a, b, P, stages, &wf);
+      l.tile_planes = (int32_t)P;
+      l.stages = stages;
+      l.seq_work_floats = (int32_t)wf;
+    }
     p->launches.push_back(l);
   }
 }
@@ -512,25 +584,26 @@ void fill_info(bs_plan* p, const std::vector<Shape4>& shapes, int n_layers, int 
   const Shape4& o = shapes.back();
   I.out = bs_shape{o.n, o.c, o.h, o.w};
   I.n_layers = n_layers;
-  I.n_steps = (int32_t)p->launches.size();
-  I.n_sequences = I.n_steps;
-  I.n_launches = I.n_steps;
+  I.n_steps = (int32_t)p->steps.size();
+  I.n_sequences = (int32_t)p->launches.size();
+  I.n_launches = I.n_sequences;
   I.n_inputs = n_inputs;
   int n_ops = 0;
   int64_t params = 0, inter = 0;
-  for (auto& l : p->launches) {
-    n_ops += (int)(l.step.pro.size() + l.step.epi.size()) + (l.step.has_pool ? 1 : 0);
-    for (auto* v : {&l.step.pro, &l.step.epi})
+  for (auto& st : p->steps) {
+    n_ops += (int)(st.pro.size() + st.epi.size()) + (st.has_pool ? 1 : 0);
+    for (auto* v : {&st.pro, &st.epi})
       for (auto& op : *v) params += (int64_t)op.affine.size() * 8;
-    if (l.dst >= 0) inter = std::max<int64_t>(inter, l.step.out.numel() * 4);
   }
+  for (auto& l : p->launches)
+    if (l.dst >= 0) inter = std::max<int64_t>(inter, l.step.out.numel() * 4);
   I.n_ops = n_ops;
   I.param_bytes = params;
   I.intermediate_bytes = p->launches.size() > 2 ? 2 * inter : inter;
   // algorithmic bytes: one read of the stack input + every ADD operand, one write of the output
   int64_t rd = shapes[0].numel() * 4;
-  for (auto& l : p->launches)
-    for (auto* v : {&l.step.pro, &l.step.epi})
+  for (auto& st : p->steps)
+    for (auto* v : {&st.pro, &st.epi})
       for (auto& op : *v)
         if (op.kind == DOP_ADD) rd += shapes[op.layer].numel() * 4;
   I.alg_bytes_read = rd;
@@ -558,6 +631,15 @@ void fill_launch_info(bs_plan* p) {
     if (l.kernel == K_EW) {
       li.grid = ew_grid(std::min<int64_t>(s.in.numel(), kEwMaxElems));
       li.n_tasks = 0;
+    } else if (l.kernel == K_SEQ) {
+      li.n_prologue_ops = (int32_t)l.seq.front().pro.size();
+      li.n_epilogue_ops = (int32_t)l.seq.back().epi.size();
+      li.groups_per_warp = (int32_t)l.seq.size();          // steps fused in the sequence
+      li.outputs_per_group = l.tile_planes;                 // planes per staged tile
+      li.rows_per_task = (int32_t)s.out.h;
+      li.n_tasks = (n_planes + l.tile_planes - 1) / l.tile_planes;
+      li.grid = (int)std::min<int64_t>(li.n_tasks, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
+      li.block = kStagedThreads;
     } else {
       li.groups_per_warp = l.G;
       li.outputs_per_group = l.Jg;
@@ -592,7 +674,24 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
     const float* src = l.src < 0 ? inputs[0] : p->inter[l.src];
     float* dst = l.dst < 0 ? out : p->inter[l.dst];
     cudaError_t e = cudaSuccess;
-    if (l.kernel == K_EW) {
+    if (l.kernel == K_SEQ) {
+      SeqArgs a;
+      std::memset(&a, 0, sizeof a);
+      a.in = src;
+      a.out = dst;
+      a.steps = p->seq_steps + l.seq_off;
+      a.n_steps = (int32_t)l.seq.size();
+      a.C = (int32_t)s.in.c;
+      a.plane0 = img0 * s.in.c;
+      a.n_planes = (img1 - img0) * s.in.c;
+      a.tile_planes = l.tile_planes;
+      a.stages = l.stages;
+      a.n_tiles = (a.n_planes + l.tile_planes - 1) / l.tile_planes;
+      a.work_floats = l.seq_work_floats;
+      a.in_plane = (int32_t)(s.in.h * s.in.w);
+      const int grid = (int)std::min<int64_t>(a.n_tiles, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
+      e = launch_seq(a, grid, st);
+    } else if (l.kernel == K_EW) {
       EwArgs a;
       std::memset(&a, 0, sizeof a);
       a.prog = make_prog(p, s.pro);
@@ -688,6 +787,7 @@ void free_plan(bs_plan* p) {
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
     if (p->params) cudaFree(p->params);
+    if (p->seq_steps) cudaFree(p->seq_steps);
     for (float* b : p->inter)
       if (b) cudaFree(b);
     for (auto& s : p->copy_stream)
@@ -766,9 +866,19 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
           op.affine_off = n_f2;
           n_f2 += op.affine.size();
         }
+  p->steps = steps;
   pack_and_tile(p, steps, o);
   for (Launch& l : p->launches) {
-    if (l.kernel != K_EW) {
+    if (l.kernel == K_SEQ) {
+      SeqArgs probe;
+      std::memset(&probe, 0, sizeof probe);
+      probe.tile_planes = l.tile_planes;
+      probe.stages = l.stages;
+      probe.work_floats = l.seq_work_floats;
+      probe.in_plane = (int32_t)(l.step.in.h * l.step.in.w);
+      const int bps = p->host_only ? 0 : seq_max_blocks_per_sm(probe);
+      l.blocks_per_sm = bps > 0 ? bps : 1;
+    } else if (l.kernel != K_EW) {
       int bps = 0;
       if (!p->host_only) {
         PoolArgs probe = make_pool_args(p, l);
@@ -795,12 +905,40 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
     if (n_f2) {
       if ((e = cudaMalloc(&p->params, n_f2 * sizeof(float2))) != cudaSuccess) return cuda_fail("cudaMalloc(params)", e);
       std::vector<float2> host(n_f2);
-      for (Launch& l : p->launches)
-        for (auto* v : {&l.step.pro, &l.step.epi})
+      for (Step& st : p->steps)
+        for (auto* v : {&st.pro, &st.epi})
           for (HostOp& op : *v)
             if (op.kind == DOP_AFFINE) std::copy(op.affine.begin(), op.affine.end(), host.begin() + op.affine_off);
       if ((e = cudaMemcpy(p->params, host.data(), n_f2 * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess)
         return cuda_fail("cudaMemcpy(params)", e);
+    }
+    {  // device descriptors of the on-chip sequences
+      std::vector<SeqStepDev> desc;
+      for (Launch& l : p->launches) {
+        if (l.kernel != K_SEQ) continue;
+        l.seq_off = desc.size();
+        for (const Step& st : l.seq) {
+          SeqStepDev d;
+          std::memset(&d, 0, sizeof d);
+          d.H = (int32_t)st.in.h; d.W = (int32_t)st.in.w; d.Ho = (int32_t)st.out.h; d.Wo = (int32_t)st.out.w;
+          if (st.has_pool) {
+            d.kh = st.kh; d.kw = st.kw; d.sh = st.sh; d.sw = st.sw; d.ph = st.ph; d.pw = st.pw;
+            d.is_max = st.is_max; d.count_include_pad = st.cip;
+          } else {  // element-wise step: a 1x1/s1 max pool is the identity
+            d.kh = d.kw = d.sh = d.sw = 1; d.is_max = 1; d.count_include_pad = 1;
+          }
+          d.pro = make_prog(p, st.pro);
+          d.epi = make_prog(p, st.epi);
+          desc.push_back(d);
+        }
+      }
+      if (!desc.empty()) {
+        if ((e = cudaMalloc(&p->seq_steps, desc.size() * sizeof(SeqStepDev))) != cudaSuccess)
+          return cuda_fail("cudaMalloc(sequence steps)", e);
+        if ((e = cudaMemcpy(p->seq_steps, desc.data(), desc.size() * sizeof(SeqStepDev), cudaMemcpyHostToDevice)) !=
+            cudaSuccess)
+          return cuda_fail("cudaMemcpy(sequence steps)", e);
+      }
     }
     int64_t inter = 0;
     for (auto& l : p->launches)

@@ -81,7 +81,34 @@ struct PoolArgs {
 
 // Kernel variants (bs_launch_info.kernel).
 enum KernelKind : int32_t { K_EW = 1, K_POOL_SPEC = 2, K_POOL_GENERIC = 3, K_POOL_NAIVE = 4, K_POOL_VEC = 5,
-                          K_POOL_STAGED = 6 };
+                          K_POOL_STAGED = 6, K_SEQ = 7 };
+
+// ---------------------------------------------------------------- multi-step sequence (NEXT-2)
+// One step of an on-chip sequence: [prologue] pool [epilogue] on the
+// step's input planes (H x W) -> (Ho x Wo).  A step without a pool is a 1x1/s1 max pool
+// (the identity).  Held in a plan-owned device array; programs have no ADD ops.
+constexpr int kMaxSeqSteps = 16;
+struct SeqStepDev {
+  int32_t H, W, Ho, Wo;
+  int32_t kh, kw, sh, sw, ph, pw;
+  int32_t is_max, count_include_pad;
+  OpProgram pro, epi;
+};
+struct SeqArgs {
+  const float* in;          // sequence input base (plane 0)
+  float* out;               // sequence output base (plane 0)
+  const SeqStepDev* steps;  // device array of n_steps descriptors
+  int32_t n_steps;
+  int32_t C;
+  int64_t plane0, n_planes;
+  int32_t tile_planes, stages;
+  int64_t n_tiles;
+  int32_t work_floats;      // floats per work buffer (tile_planes x largest intermediate plane)
+  int32_t in_plane;         // H0 * W0
+};
+cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st);
+size_t seq_smem(const SeqArgs& a);
+int seq_max_blocks_per_sm(const SeqArgs& a);
 
 // Launchers (bs_kernels.cu).  Return the launch error (cudaSuccess on success).
 cudaError_t launch_ew(const EwArgs& a, int grid, int block, cudaStream_t st);

@@ -57,7 +57,11 @@ def test_step_grouping_paper_example(bs):
     # lst:finalcode: step_0 = MaxPooling, BatchNorm, ReLU; step_1 = AvgPooling (+AvgNormalization)
     shape = (1, 4, 16, 16)
     layers = [synth.maxpool(2, 2), synth.batchnorm(4, 1), synth.relu(), synth.avgpool(2, 2), synth.batchnorm(4, 2)]
-    p = host_plan(bs, layers, shape)
+    info = bs.bs_plan_query(host_plan(bs, layers, shape))
+    assert (info["n_steps"], info["n_sequences"]) == (2, 1)      # lst:finalcode's sequence_0
+    li = bs.bs_plan_query_launch(host_plan(bs, layers, shape), 0)
+    assert (li["kernel"], li["groups_per_warp"], li["first_layer"], li["last_layer"]) == (7, 2, 0, 4)
+    p = host_plan(bs, layers, shape, max_steps_per_sequence=1)   # one step per launch
     info = bs.bs_plan_query(p)
     assert info["n_steps"] == 2
     l0, l1 = bs.bs_plan_query_launch(p, 0), bs.bs_plan_query_launch(p, 1)
@@ -76,6 +80,27 @@ def test_step_grouping_paper_example(bs):
 def test_step_counts(bs, layers, steps):
     p = host_plan(bs, layers, (2, 3, 40, 40))
     assert bs.bs_plan_query(p)["n_steps"] == steps
+
+
+@pytest.mark.parametrize("depth,policy,seqs", [(16, 5, 4), (16, 1, 16), (16, 0, 1), (40, 0, 3), (40, 5, 8),
+                                               (1, 0, 1)])
+def test_sequence_packing(bs, depth, policy, seqs):
+    """§5.1 blocks [MaxPool3x3/s1/p1, BN, ReLU] x depth: one step per block; the paper's three
+    policies -> ceil(depth / limit) sequences (16 blocks, <= 5 -> 4)."""
+    layers = []
+    for b in range(depth):
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(8, b), synth.relu()]
+    info = bs.bs_plan_query(host_plan(bs, layers, (4, 8, 28, 28), max_steps_per_sequence=policy))
+    assert info["n_steps"] == depth and info["n_sequences"] == seqs and info["n_launches"] == seqs
+
+
+def test_sequence_respects_shared_memory(bs):
+    """Planes too large for shared memory are not fused (one step per sequence)."""
+    layers = [synth.maxpool(3, 1, 1), synth.relu(), synth.maxpool(3, 1, 1)]
+    info = bs.bs_plan_query(host_plan(bs, layers, (1, 2, 224, 224)))
+    assert info["n_sequences"] == 2
+    info = bs.bs_plan_query(host_plan(bs, layers, (1, 2, 56, 56)))
+    assert info["n_sequences"] == 1
 
 
 def test_copy_is_elided(bs):

@@ -175,7 +175,9 @@ def test_random_stacks(trial, cuda_dev, oracle_lib):
                                    max_pools=rng.choice([1, 2, 4]), seed_base=60000 + 50 * trial)
     shapes = oracle.layer_shapes(layers, shape, n_ops)
     x, ops = U.make_inputs(layers, shape, n_ops, 123 + trial, shapes)
-    compare(layers, x, ops, ctx=f"trial {trial} {[L.kind for L in layers]} {shape}")
+    for policy in (0, 1):   # on-chip sequences and one launch per step
+        compare(layers, x, ops, opts={"max_steps_per_sequence": policy},
+                ctx=f"trial {trial} policy {policy} {[L.kind for L in layers]} {shape}")
 
 
 def test_multi_sequence_stack(cuda_dev, oracle_lib):
@@ -189,7 +191,33 @@ def test_multi_sequence_stack(cuda_dev, oracle_lib):
     x = synth.uniform_np(77, int(np.prod(shape))).reshape(shape)
     got, plan = compare(layers, x, ctx="multi")
     info = bs.bs_plan_query(plan)
-    assert info["n_steps"] == 7 and info["n_launches"] == 7
+    assert info["n_steps"] == 7 and info["n_launches"] == 1       # one on-chip sequence
+    for policy, launches in ((1, 7), (5, 2), (2, 4)):
+        g2, p2 = compare(layers, x, opts={"max_steps_per_sequence": policy}, ctx=f"policy {policy}")
+        assert bs.bs_plan_query(p2)["n_launches"] == launches
+        U.assert_close(g2, got, f"policy {policy} vs one sequence")   # avg sums differ in order
+
+
+@pytest.mark.parametrize("depth", [1, 2, 5, 16, 17, 40])
+def test_sec51_blocks(depth, cuda_dev, oracle_lib):
+    """PAPER.md §5.1: 1-40 blocks of MaxPool3x3/s1/p1 -> BN -> ReLU, under the
+    three sequence policies (1 step, <= 5 steps, unlimited)."""
+    bs = _bs()
+    shape = (2, 3, 20, 20)
+    layers = []
+    for b in range(depth):
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(3, 300 + b), synth.relu()]
+    x = synth.uniform_np(depth, int(np.prod(shape))).reshape(shape)
+    ref = oracle.run_bf(layers, x)
+    outs = []
+    for policy in (1, 5, 0):
+        got, plan = run_gpu(layers, x, opts={"max_steps_per_sequence": policy})
+        U.assert_close(got, ref, f"depth {depth} policy {policy}")
+        outs.append(got)
+        n = bs.bs_plan_query(plan)["n_launches"]
+        assert n == {1: depth, 5: -(-depth // 5), 0: -(-depth // 16)}[policy], (policy, n)
+    U.assert_bitexact(outs[1], outs[0], "policy 5 vs 1")
+    U.assert_bitexact(outs[2], outs[0], "unlimited vs 1")
 
 
 def test_long_elementwise_runs_split(cuda_dev, oracle_lib):
