@@ -14,6 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libbrainslug.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+OBJ_DIR = os.path.join(PKG, "build")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -30,7 +31,7 @@ def sources():
 
 
 def deps():
-    return sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "bs.h"), __file__]
+    return sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "bs.h"), __file__]
 
 
 def stale() -> bool:
@@ -40,11 +41,37 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
+def _compile(src: str, obj: str, verbose: bool) -> None:
+    flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+    cmd = [NVCC, *flags, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit (in parallel) and link libbrainslug.so."""
     if not (force or stale()):
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    headers = [p for p in deps() if p.endswith((".h", ".cuh", ".py"))]
+    newest_hdr = max(os.path.getmtime(p) for p in headers)
+    jobs, objs = [], []
+    for src in sources():
+        obj = os.path.join(OBJ_DIR, os.path.basename(src) + f".{os.getpid()}.o")
+        final = os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
+        objs.append(final)
+        if force or not os.path.exists(final) or os.path.getmtime(final) < max(os.path.getmtime(src), newest_hdr):
+            jobs.append((src, obj, final))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+        for f in [ex.submit(_compile, s_, o_, verbose) for s_, o_, _ in jobs]:
+            f.result()
+    for _, o_, fin in jobs:
+        os.replace(o_, fin)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+           "-Xcompiler", "-fPIC", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)

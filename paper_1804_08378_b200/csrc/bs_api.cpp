@@ -297,34 +297,52 @@ void set_device_programs(Launch& l) {
   l.deferred = true;
 }
 
-// Staged-kernel tile: P whole planes (P*H*W*4 bytes, a multiple of 16 for the bulk copy),
-// at most kStagedTileMax bytes, preferring a task count that splits evenly over the
-// consumer warps; ring depth so that two CTAs fit one SM.  False if a plane is too big.
-constexpr int64_t kStagedTileMax = 48 * 1024;
-constexpr int64_t kStagedTileMin = 8 * 1024;
+// Staged-kernel tile (k_pool_staged.cu): P whole planes per tile and bands of R output rows,
+// chosen so that the 8 consumer warps share every tile evenly.  A tile holds I =
+// ceil(P/G) * n_cc * ceil(Ho/R) items and each warp walks ceil(I/8) of them in turn, each item
+// reducing R*s + (k-s) input rows; the choice minimises that per-tile walk per staged plane,
+// (I <= 16: a warp holds at most two items), with a mild preference for 12-32 KB tiles (small enough for >= 3 ring stages at two CTAs per
+// SM and for the last tile of a CTA's range to be cheap; large enough to amortise the per-tile
+// barrier work).  Ring depth: as many stages as fit two CTAs per SM (<= 8).  False if one
+// plane group is too large to stage.
+constexpr int64_t kStagedTileMax = 32 * 1024;
 constexpr int64_t kStagedSmemPerCta = 110 * 1024;   // two CTAs per SM
 bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_sms) {
-  const int64_t HW = l.step.in.h * l.step.in.w;
-  // tiles of whole planes (any count: head/tail floats of unaligned tiles are copied by the
-  // producer lane), a multiple of the G planes a warp covers; ~8 tiles per CTA or more,
-  // within [8 KB, 48 KB]; as many ring stages as fit two CTAs per SM
-  const int step = l.G;
-  const int64_t total = n_planes * HW * 4;
-  const int64_t want = std::max(kStagedTileMin, std::min(kStagedTileMax, total / (16 * (int64_t)num_sms)));
-  int64_t P = std::max<int64_t>(step, want / (HW * 4) / step * step);
-  P = std::min(P, (n_planes + step - 1) / step * step);
-  if (o.force_tile_planes > 0) P = std::max<int64_t>(step, (int64_t)o.force_tile_planes / step * step);
-  const int64_t stride = (int64_t)pool_staged_stride((int)P, (int)HW);
+  (void)num_sms;
+  const Step& st = l.step;
+  const int64_t HW = st.in.h * st.in.w, Ho = st.out.h;
+  const int64_t plane_bytes = HW * 4;
+  const int64_t G = l.G, ncc = l.n_cc, NC = kStagedConsumerWarps;
+  const int64_t carry = std::max(0, st.kh - st.sh);
+  const int64_t max_groups = (n_planes + G - 1) / G;
+  double best = 1e300;
+  int64_t bP = G, bR = Ho;
+  for (int64_t m = 1; m <= max_groups && (m == 1 || m * G * plane_bytes <= kStagedTileMax); ++m) {
+    if (o.force_tile_planes > 0 && m != std::max<int64_t>(1, o.force_tile_planes / G)) continue;
+    for (int64_t R = 1; R <= Ho; ++R) {
+      const int64_t nrb = (Ho + R - 1) / R;
+      if (R > 1 && (Ho + R - 2) / (R - 1) == nrb) continue;     // same band count as R-1
+      if (o.force_rows_per_task > 0 && R != std::min<int64_t>(Ho, o.force_rows_per_task)) continue;
+      const int64_t I = m * ncc * nrb;
+      if (I > 2 * NC) continue;                                  // the kernel holds <= 2 items per warp
+      const double walk = (double)((I + NC - 1) / NC) * (double)(R * st.sh + carry);
+      const int64_t T = m * G * plane_bytes;
+      const double size_f = T < 8192 ? 1.25 : T < 12288 ? 1.05 : T > kStagedTileMax ? 1.1 : 1.0;
+      const double cost = walk / (double)(m * G) * size_f;
+      if (cost < best * (1 - 1e-9)) { best = cost; bP = m * G; bR = R; }
+    }
+  }
+  const int64_t stride = (int64_t)pool_staged_stride((int)bP, (int)HW);
+  const int64_t obufs = 0;
   if (stride > 100 * 1024) return false;   // plane group too large to stage
-  l.tile_planes = (int32_t)P;
-  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(8, kStagedSmemPerCta / stride));
-  if (o.force_stages >= 2) l.stages = std::min(8, o.force_stages);
-  if ((int64_t)l.stages * stride > 220 * 1024) l.stages = (int32_t)((220 * 1024) / stride);
+  l.tile_planes = (int32_t)bP;
+  l.rows_per_task = (int32_t)bR;
+  l.n_rb = (int32_t)((Ho + bR - 1) / bR);
+  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kStagedMaxStages, (kStagedSmemPerCta - obufs) / stride));
+  if (o.force_stages >= 2) l.stages = std::min(kStagedMaxStages, o.force_stages);
+  if ((int64_t)l.stages * stride + obufs > 220 * 1024) l.stages = (int32_t)((220 * 1024 - obufs) / stride);
   if (l.stages < 2) return false;
-  l.U = pool_staged_unroll(l.step.kh, l.step.sh);
-  const int64_t Ho = l.step.out.h;
-  l.rows_per_task = (int32_t)(o.force_rows_per_task > 0 ? std::min<int64_t>(Ho, o.force_rows_per_task) : Ho);
-  l.n_rb = (int32_t)((Ho + l.rows_per_task - 1) / l.rows_per_task);
+  l.U = 1;
   return true;
 }
 
@@ -555,6 +573,7 @@ PoolArgs make_pool_args(const bs_plan* p, const Launch& l) {
   a.epi_class = prog_class(l.dev_epi);
   a.tile_planes = l.tile_planes;
   a.stages = l.stages;
+  a.cdiv = make_fastdiv((uint32_t)a.C);
   return a;
 }
 

@@ -1,5 +1,5 @@
 // bs_internal.h -- shared between the host planner/runtime (bs_api.cpp) and the sm_100a
-// kernels (bs_kernels.cu).  Not part of the public ABI (see include/bs.h).
+// kernels (k_*.cu, bs_device.cuh).  Not part of the public ABI (see include/bs.h).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -76,6 +76,7 @@ struct PoolArgs {
   int32_t tile_planes;      // planes per tile (tile_planes * H * W % 4 == 0)
   int32_t stages;           // shared-memory ring depth
   int64_t n_tiles;          // ceil(n_planes / tile_planes)
+  FastDiv cdiv;             // channels C (plane -> channel)
   OpProgram pro, epi;       // prologue (per input element), epilogue (per output element)
 };
 
@@ -110,7 +111,7 @@ cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st);
 size_t seq_smem(const SeqArgs& a);
 int seq_max_blocks_per_sm(const SeqArgs& a);
 
-// Launchers (bs_kernels.cu).  Return the launch error (cudaSuccess on success).
+// Launchers (k_*.cu).  Return the launch error (cudaSuccess on success).
 cudaError_t launch_ew(const EwArgs& a, int grid, int block, cudaStream_t st);
 cudaError_t launch_pool(const PoolArgs& a, int kernel_kind, int grid, int block, cudaStream_t st);
 // Whether a specialised (compile-time k/s) column-walker exists for this geometry.
@@ -128,8 +129,13 @@ int pool_vec_unroll(int vec);
 #endif
 constexpr int kStagedConsumerWarps = BS_STAGED_CW;
 constexpr int kStagedThreads = 32 * (kStagedConsumerWarps + 1);
-size_t pool_staged_smem(int tile_planes, int HW, int stages);
-__host__ __device__ size_t pool_staged_stride(int tile_planes, int HW);
+constexpr int kStagedMaxStages = 8;    // mbarrier pairs in the staged kernels' smem header
+constexpr int kStagedHeader = 128;     // bytes of smem before the first stage
+size_t pool_staged_smem(int tile_planes, int HW, int HWo, int stages);
+// Bytes of one ring stage: a tile of P planes at offset (global address mod 16), 128-B multiple.
+__host__ __device__ inline size_t pool_staged_stride(int tile_planes, int HW) {
+  return ((size_t)tile_planes * HW * 4 + 16 + 127) / 128 * 128;
+}
 int pool_staged_unroll(int k, int s);
 int pool_max_blocks_per_sm(int kernel_kind, const PoolArgs& a, int block);
 

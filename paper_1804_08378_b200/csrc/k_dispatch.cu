@@ -1,0 +1,67 @@
+// k_dispatch.cu -- host-side kernel selection and launch helpers.
+#include "bs_device.cuh"
+
+namespace bs {
+
+
+FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t s = 0;
+  while (s < 32 && (uint64_t(1) << s) < d) ++s;
+  f.s = s;
+  f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << s) - d)) / d + 1);
+  return f;
+}
+
+
+static void* pool_fn(int kind, const PoolArgs& a) {
+  return kind == K_POOL_STAGED ? pool_fn_staged(a) : pool_fn_global(kind, a);
+}
+
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+cudaError_t launch_pool(const PoolArgs& a, int kind, int grid, int block, cudaStream_t st) {
+  (void)block;
+  void* fn = pool_fn(kind, a);
+  if (!fn) return cudaErrorInvalidDeviceFunction;
+  void* args[] = {(void*)&a};
+  if (kind == K_POOL_STAGED) {
+    const size_t smem = pool_staged_smem(a.tile_planes, a.H * a.W, a.Ho * a.Wo, a.stages);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(fn, dim3(grid), dim3(kStagedThreads), args, smem, st);
+  }
+  return launch_pdl(fn, dim3(grid), dim3(kPoolBlock), args, 0, st);
+}
+
+
+int pool_max_blocks_per_sm(int kind, const PoolArgs& a, int block) {
+  (void)block;
+  void* fn = pool_fn(kind, a);
+  int n = 0;
+  if (!fn) return 0;
+  if (kind == K_POOL_STAGED) {
+    const size_t smem = pool_staged_smem(a.tile_planes, a.H * a.W, a.Ho * a.Wo, a.stages);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kStagedThreads, smem) != cudaSuccess) n = 0;
+    return n;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kPoolBlock, 0) != cudaSuccess) n = 0;
+  return n;
+}
+
+
+}  // namespace bs

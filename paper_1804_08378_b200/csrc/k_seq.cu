@@ -1,0 +1,154 @@
+// k_seq.cu -- on-chip multi-step sequences (NEXT-2).
+#include "bs_device.cuh"
+
+namespace bs {
+
+// ------------------------------------------------------------------ multi-step sequences
+//
+// NEXT-2: a *sequence* of several steps runs on-chip (PAPER.md P:L545-558,
+// lst:finalcode P:L512-530 "float cached_data[...]"; the paper's GPU kernel swapped two smem
+// buffers per step).  A tile of P whole planes is bulk-copied (TMA) into the ring
+// as in pool_staged; step 0 reads the stage buffer, every later step reads the previous step's
+// work buffer (two ping-pong buffers in shared memory), and only the last step writes HBM.
+// Whole planes mean no halo growth with depth.  The 8 consumer warps split each step's
+// output rows; a named barrier (bar.sync 1, 256) separates steps.
+
+size_t seq_smem(const SeqArgs& a) {
+  return 128 + (size_t)a.stages * pool_staged_stride(a.tile_planes, a.in_plane) + 2 * (size_t)a.work_floats * 4 + 256;
+}
+
+// One output element of a step from a smem plane (padding absent for max / zero for avg).
+__device__ __forceinline__ float seq_window(const SeqStepDev& st, const float* pl, int i, int j, int ch,
+                                            const float2 (&paff)[kAffSlots]) {
+  const bool is_max = st.is_max != 0;
+  float acc = is_max ? -CUDART_INF_F : 0.f;
+  int real = 0;
+  const int r0 = i * st.sh - st.ph, q0 = j * st.sw - st.pw;
+  for (int u = 0; u < st.kh; ++u) {
+    const int r = r0 + u;
+    if ((unsigned)r >= (unsigned)st.H) continue;
+    const float* row = pl + r * st.W;
+    for (int v = 0; v < st.kw; ++v) {
+      const int q = q0 + v;
+      if ((unsigned)q >= (unsigned)st.W) continue;
+      float x = row[q];
+      if (st.pro.n) x = apply_generic(st.pro, paff, ch, x, 0);
+      acc = is_max ? fmaxf(acc, x) : __fadd_rn(acc, x);
+      ++real;
+    }
+  }
+  if (!is_max) acc = __fdiv_rn(acc, st.count_include_pad ? (float)(st.kh * st.kw) : (float)real);
+  return acc;
+}
+
+__global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = (uint64_t*)smem;
+  uint64_t* empty = full + 8;
+  const size_t tile_stride = pool_staged_stride(a.tile_planes, a.in_plane);
+  unsigned char* stage0 = smem + 128;
+  float* work[2] = {(float*)(stage0 + (size_t)a.stages * tile_stride),
+                    (float*)(stage0 + (size_t)a.stages * tile_stride) + a.work_floats};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (int)a.n_tiles;
+  const int HW0 = a.in_plane;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();                   // previous kernel on the stream complete + visible
+  pdl_launch_dependents();
+
+  if (warp == 0) {  // producer, as in pool_staged
+    if (lane == 0) {
+      int k = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+        const int s = k % a.stages;
+        if (k >= a.stages) mbar_wait(&empty[s], ((k / a.stages) - 1) & 1);
+        const int64_t pl0 = (int64_t)t * a.tile_planes;
+        const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
+        const float* src = a.in + (a.plane0 + pl0) * (int64_t)HW0;
+        const uint32_t head_off = (uint32_t)((uintptr_t)src & 15u);
+        float* dst = (float*)((char*)stage0 + (size_t)s * tile_stride + head_off);
+        const uint32_t nbytes = (uint32_t)np * (uint32_t)HW0 * 4u;
+        const uint32_t h = min(nbytes, (16u - head_off) & 15u);
+        const uint32_t body = (nbytes - h) & ~15u;
+        for (uint32_t e = 0; e < h / 4; ++e) cp_async4(dst + e, src + e);
+        for (uint32_t e = (h + body) / 4; e < nbytes / 4; ++e) cp_async4(dst + e, src + e);
+        cp_async_mbar_arrive(&full[s]);
+        if (body) {
+          mbar_arrive_expect_tx(&full[s], body);
+          for (uint32_t off = 0; off < body; off += kBulkChunk)
+            bulk_g2s((char*)dst + h + off, (const char*)src + h + off, min(kBulkChunk, body - off), &full[s]);
+        } else {
+          mbar_arrive(&full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  const int cw = warp - 1;   // consumer warp 0..7
+  int k = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+    const int s = k % a.stages;
+    mbar_wait(&full[s], (k / a.stages) & 1);
+    const int64_t pl0 = (int64_t)t * a.tile_planes;
+    const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
+    const float* src_base = (const float*)((const char*)stage0 + (size_t)s * tile_stride +
+                                           ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW0) & 15u));
+    for (int st_i = 0; st_i < a.n_steps; ++st_i) {
+      const SeqStepDev& st = a.steps[st_i];
+      const bool last = st_i == a.n_steps - 1;
+      const float* in_buf = st_i == 0 ? src_base : work[(st_i - 1) & 1];
+      float* out_buf = work[st_i & 1];
+      const int HWi = st.H * st.W, HWo = st.Ho * st.Wo;
+      // work items: (plane, output row, 32-column chunk); lane = output column
+      const int nchunk = (st.Wo + 31) / 32;
+      const int items = np * st.Ho * nchunk;
+      for (int it = cw; it < items; it += kStagedConsumerWarps) {
+        const int cc = it % nchunk;
+        const int i = (it / nchunk) % st.Ho;
+        const int p = it / (nchunk * st.Ho);
+        const int j = cc * 32 + lane;
+        if (j >= st.Wo) continue;
+        const int64_t plane = a.plane0 + pl0 + p;
+        const int ch = (int)(plane % a.C);
+        float2 paff[kAffSlots], eaff[kAffSlots];
+        load_affine(st.pro, ch, paff);
+        load_affine(st.epi, ch, eaff);
+        float r = seq_window(st, in_buf + p * HWi, i, j, ch, paff);
+        r = apply_generic(st.epi, eaff, ch, r, 0);
+        if (last) __stcs(a.out + plane * (int64_t)HWo + i * st.Wo + j, r);
+        else out_buf[p * HWo + i * st.Wo + j] = r;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kStagedConsumerWarps) : "memory");   // step boundary
+      if (st_i == 0 && cw == 0 && lane == 0) mbar_arrive(&empty[s]);   // stage buffer consumed
+    }
+  }
+}
+
+cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st) {
+  void* args[] = {(void*)&a};
+  const size_t smem = seq_smem(a);
+  cudaError_t e = cudaFuncSetAttribute((void*)seq_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl((void*)seq_staged, dim3(grid), dim3(kStagedThreads), args, smem, st);
+}
+
+int seq_max_blocks_per_sm(const SeqArgs& a) {
+  const size_t smem = seq_smem(a);
+  int n = 0;
+  if (cudaFuncSetAttribute((void*)seq_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, (void*)seq_staged, kStagedThreads, smem) != cudaSuccess) n = 0;
+  return n;
+}
+
+
+}  // namespace bs
