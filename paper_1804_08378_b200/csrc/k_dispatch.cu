@@ -29,7 +29,11 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
+#ifdef BS_NO_PDL
+  cfg.numAttrs = 0;
+#else
   cfg.numAttrs = 1;
+#endif
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
