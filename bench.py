@@ -35,7 +35,8 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 METRIC = "fused-stack HBM GB/s (% of B200 peak) and images/sec at 1/2/4/8 GPUs"
-CONFIG_INDEX = {"c1": 0, "alexnet": 1, "vgg16": 2, "resnet50": 3, "densenet121": 4}
+CONFIG_INDEX = {"c1": 0, "alexnet": 1, "vgg16": 2, "resnet50": 3, "densenet121": 4,
+                "resnet50_residual": None}   # NEXT-1: not a BASELINE config
 
 
 def load_peaks():
@@ -117,8 +118,10 @@ def time_oracle(cases, budget_s: float, max_images: int):
         for c in cases:
             shp = (1,) + tuple(c.shape[1:])
             x = synth.uniform_np(c.input_seed, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
+            ops = [synth.uniform_np(sd, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
+                   for sd in c.operand_seeds]
             for _ in range(c.count):
-                oracle.run_bf(c.layers, x)
+                oracle.run_bf(c.layers, x, ops)
     t0 = time.perf_counter()
     one_image(0)
     t1 = time.perf_counter() - t0
@@ -142,8 +145,10 @@ def run_reference(args):
         for c in cases:
             shp = (1,) + tuple(c.shape[1:])
             x = synth.uniform_np(c.input_seed, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
+            ops = [synth.uniform_np(sd, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
+                   for sd in c.operand_seeds]
             for _ in range(c.count):
-                oracle.run_bf(c.layers, x)
+                oracle.run_bf(c.layers, x, ops)
     for k in range(args.warmup):
         step(k)
     t0 = time.perf_counter()
@@ -230,8 +235,10 @@ def main():
         row = []
         for j, c in enumerate(inst):
             x = synth.uniform_torch(c.input_seed + 7 * j, c.shape, device=dev, start=rank * int(np.prod(c.shape)))
+            ops = [synth.uniform_torch(sd + 7 * j, c.shape, device=dev, start=rank * int(np.prod(c.shape)))
+                   for sd in c.operand_seeds]       # ADD operands (NEXT-1 residual stacks)
             y = torch.empty(infos[c.name]["out"], device=dev)
-            row.append((x, y))
+            row.append(([x] + ops, y))
         bufs.append(row)
     # dominant instance: the most algorithmic bytes
     dom = max(range(len(inst)), key=lambda j: infos[inst[j].name]["alg_bytes_read"] + infos[inst[j].name]["alg_bytes_written"])
@@ -242,11 +249,17 @@ def main():
     sh = stream.cuda_stream
     handles = [plans[c.name] for c in inst]
 
+    def launch(h, xs, y, st_handle):
+        if len(xs) == 1:
+            bs.bs_execute(h, xs[0].data_ptr(), y.data_ptr(), st_handle)
+        else:
+            bs.bs_execute_ex(h, [t.data_ptr() for t in xs], y.data_ptr(), st_handle)
+
     def step(k, st_handle):
         row = bufs[k % n_sets]
         for j, h in enumerate(handles):
-            x, y = row[j]
-            bs.bs_execute(h, x.data_ptr(), y.data_ptr(), st_handle)
+            xs, y = row[j]
+            launch(h, xs, y, st_handle)
 
     # eager warm-up (also JIT-loads every kernel), then one CUDA graph per buffer set so the
     # timed region measures the device, not the Python launch loop
@@ -294,14 +307,15 @@ def main():
     D = max(4, min(50, int(4 * l2 // max(1, dom_bytes)) + 4))
     dom_sets = max(n_sets, int(math.ceil(4 * l2 / dom_bytes)) + 1)
     dbufs = [bufs[sidx % n_sets][dom] if sidx < n_sets else
-             (synth.uniform_torch(inst[dom].input_seed + 99 * sidx, inst[dom].shape, device=dev),
+             ([synth.uniform_torch(sd + 99 * sidx, inst[dom].shape, device=dev)
+               for sd in [inst[dom].input_seed] + inst[dom].operand_seeds],
               torch.empty(infos[inst[dom].name]["out"], device=dev)) for sidx in range(dom_sets)]
     dh = handles[dom]
 
     def dom_burst(st_handle):
         for r in range(D):
-            x, y = dbufs[r % dom_sets]
-            bs.bs_execute(dh, x.data_ptr(), y.data_ptr(), st_handle)
+            xs, y = dbufs[r % dom_sets]
+            launch(dh, xs, y, st_handle)
 
     with torch.cuda.stream(stream):
         dom_burst(sh)
@@ -346,15 +360,15 @@ def main():
         for c in cases:
             nb = infos[c.name]["alg_bytes_read"] + infos[c.name]["alg_bytes_written"]
             nset = int(math.ceil(4 * l2 / nb)) + 1
-            sb = [(synth.uniform_torch(c.input_seed + 13 * q, c.shape, device=dev),
+            sb = [([synth.uniform_torch(sd + 13 * q, c.shape, device=dev) for sd in [c.input_seed] + c.operand_seeds],
                    torch.empty(infos[c.name]["out"], device=dev)) for q in range(min(nset, 64))]
             R = max(8, min(64, len(sb) * 2))
             hh = plans[c.name]
 
             def burst(st_handle):
                 for r in range(R):
-                    x, y = sb[r % len(sb)]
-                    bs.bs_execute(hh, x.data_ptr(), y.data_ptr(), st_handle)
+                    xs, y = sb[r % len(sb)]
+                    launch(hh, xs, y, st_handle)
             with torch.cuda.stream(stream):
                 burst(sh)
             torch.cuda.synchronize()
@@ -378,7 +392,7 @@ def main():
     # ---- end to end: host buffers through bs_execute_host (H2D + kernels + D2H every step)
     e2e = None
     e2e_steps = args.e2e_steps or max(3, min(20, args.steps // 10))
-    max_in = max(infos[c.name]["alg_bytes_read"] for c in cases) // 4
+    max_in = max(infos[c.name]["alg_bytes_read"] // (1 + len(c.operand_seeds)) for c in cases) // 4
     max_out = max(infos[c.name]["alg_bytes_written"] for c in cases) // 4
     h_in = torch.empty(max_in, dtype=torch.float32).pin_memory()
     h_in.copy_(synth.uniform_torch(99, (max_in,), device=dev).cpu())
@@ -389,8 +403,10 @@ def main():
     def e2e_step(k):
         row = bufs[k % n_sets]
         for j, h in enumerate(handles):
-            x, y = row[j]
-            bs.bs_execute_host(h, [h_in.data_ptr()], h_out.data_ptr(), [x.data_ptr()], y.data_ptr(), 0, sh)
+            xs, y = row[j]
+            # every input (stack input and ADD operands) is copied from pinned host memory
+            bs.bs_execute_host(h, [h_in.data_ptr()] * len(xs), h_out.data_ptr(), [t.data_ptr() for t in xs],
+                               y.data_ptr(), 0, sh)
 
     e2e_step(0)
     torch.cuda.synchronize()
@@ -425,7 +441,8 @@ def main():
         def lbl_step(k):
             row = bufs[k % n_sets]
             for j, c in enumerate(inst):
-                t = row[j][0]
+                xs = row[j][0]
+                t = xs[0]
                 for L, p in zip(c.layers, params[c.name]):
                     if L.kind == "batchnorm":
                         t = F.batch_norm(t, p[0], p[1], p[2], p[3], False, 0.0, L.eps)
@@ -435,6 +452,8 @@ def main():
                         t = F.max_pool2d(t, L.kernel, L.stride, L.padding)
                     elif L.kind == "avgpool":
                         t = F.avg_pool2d(t, L.kernel, L.stride, L.padding, count_include_pad=L.count_include_pad)
+                    elif L.kind == "add":
+                        t = t + xs[L.operand]
         lsteps = max(3, min(50, args.steps // 4))
         with torch.cuda.stream(stream):
             for k in range(3):
@@ -453,9 +472,9 @@ def main():
     # ---- CPU oracle baseline on a bounded sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, n, T = time_oracle(cases, args.cpu_budget, batch)
+        v, n, T = time_oracle(cases, args.cpu_budget, 1 << 20)
         cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle",
-               "sample": f"{n} images of the batch-{batch} {args.workload} workload (all stacks), "
+               "sample": f"{n} synthetic images shaped like the batch-{batch} {args.workload} workload (all stacks), "
                          f"breadth-first C oracle, single thread, {T:.1f} s"}
 
     traffic = None

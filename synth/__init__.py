@@ -257,10 +257,22 @@ def workload(name: str, batch: Optional[int] = None) -> List[StackCase]:
         sb = seed_for(cfg, si, 0)
         cases.append(StackCase("densenet121_final", (N, 1024, 7, 7),
                                _bn_relu(1024, sb) + [avgpool(7, 7)], sb))
+    elif name == "resnet50_residual":
+        # NEXT-1: the bottleneck tail bn3 -> (+ identity) -> ReLU of every
+        # ResNet-50 block, a two-input stack (ADD operand 1 = the block's shortcut)
+        cfg, N = 3, batch or 256
+        si = 100
+        for (C, H, cnt) in [(256, 56, 3), (512, 28, 4), (1024, 14, 6), (2048, 7, 3)]:
+            sb = seed_for(cfg, si, 0)
+            cases.append(StackCase(f"resnet50_tail_{C}x{H}", (N, C, H, H),
+                                   [batchnorm(C, sb), add(1), relu()], sb,
+                                   operand_seeds=[seed_for(cfg, si, 5)], count=cnt))
+            si += 1
     else:
         raise ValueError(f"unknown workload {name!r}")
     return cases
 
 
-WORKLOADS = ("c1", "alexnet", "vgg16", "resnet50", "densenet121")
-DEFAULT_BATCH = {"c1": 1, "alexnet": 128, "vgg16": 64, "resnet50": 256, "densenet121": 256}
+WORKLOADS = ("c1", "alexnet", "vgg16", "resnet50", "densenet121", "resnet50_residual")
+DEFAULT_BATCH = {"c1": 1, "alexnet": 128, "vgg16": 64, "resnet50": 256, "densenet121": 256,
+                 "resnet50_residual": 256}

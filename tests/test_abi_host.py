@@ -114,9 +114,10 @@ def test_alg_bytes_match_survey(bs, wl):
     for case in synth.workload(wl):
         p = host_plan(bs, case.layers, case.shape)
         info = bs.bs_plan_query(p)
-        oshape = oracle.layer_shapes(case.layers, case.shape)[-1]
+        oshape = oracle.layer_shapes(case.layers, case.shape, len(case.operand_seeds))[-1]
         assert info["out"] == oshape
-        assert info["alg_bytes_read"] == 4 * int(np.prod(case.shape))
+        # (+ one read of each ADD operand: the NEXT-1 residual stacks)
+        assert info["alg_bytes_read"] == 4 * int(np.prod(case.shape)) * (1 + len(case.operand_seeds))
         assert info["alg_bytes_written"] == 4 * int(np.prod(oshape))
         assert info["n_launches"] == 1
     c3 = synth.workload("vgg16")[0]

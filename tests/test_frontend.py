@@ -1,0 +1,98 @@
+"""NEXT-4 front-end (paper_1804_08378_b200/frontend.py): stack detection in torchvision graphs.
+
+CPU: the optimizable-layer and stack counts of the paper's tbl:eval_detailkernel networks, as
+reconciled in SURVEY.md Appendix A (FX graphs of torchvision 0.26 architectures, no weights),
+and the structure of an optimized graph.  GPU: an optimized network equals the eager network.
+"""
+import pytest
+import torch
+
+torchvision = pytest.importorskip("torchvision")
+
+# SURVEY.md Appendix A, column "ours" (the paper's Opt. column agrees for every net; its Stacks
+# column has one more stack for the ResNets, App. A's reading: a separate final AvgPool stack)
+APPENDIX_A = {"alexnet": (12, 8), "vgg11": (17, 10), "vgg16": (22, 15), "vgg16_bn": (35, 15),
+              "densenet121": (247, 124), "densenet161": (327, 164), "resnet18": (39, 20),
+              "resnet50": (104, 53), "resnet152": (308, 155)}
+
+
+@pytest.mark.parametrize("net", sorted(APPENDIX_A))
+def test_counts_match_appendix_a(net):
+    from paper_1804_08378_b200 import frontend as fe
+    d = fe.summary(getattr(torchvision.models, net)().eval())
+    assert (d["opt_layers"], d["stacks"]) == APPENDIX_A[net]
+
+
+def test_stack_signatures():
+    """Appendix A's per-network stack lists."""
+    from paper_1804_08378_b200 import frontend as fe
+    sig = fe.summary(torchvision.models.alexnet().eval())["signatures"]
+    assert sig == ["[relu,maxpool]"] * 2 + ["[relu]"] * 2 + ["[relu,maxpool]", "[copy]", "[relu,copy]", "[relu]"]
+    sig = fe.summary(torchvision.models.resnet50().eval())["signatures"]
+    assert sig[0] == "[batchnorm,relu,maxpool]"
+    assert sig.count("[batchnorm,add,relu]") == 15 and sig[-1] == "[batchnorm,add,relu,avgpool]"
+    assert sig.count("[batchnorm]") == 4                                  # down-sample branches
+    sig = fe.summary(torchvision.models.densenet121().eval())["signatures"]
+    assert sig[0] == "[batchnorm,relu,maxpool]" and sig[-1] == "[batchnorm,relu,avgpool]"
+    assert sig.count("[avgpool]") == 3                                    # transition pools
+
+
+def test_optimized_graph_structure():
+    from paper_1804_08378_b200 import frontend as fe
+    m = torchvision.models.resnet18().eval()
+    gm = fe.optimize(m)
+    stacks = [mod for mod in gm.modules() if isinstance(mod, fe.BrainSlugStack)]
+    assert len(stacks) == 20
+    called = [gm.get_submodule(n.target) for n in gm.graph.nodes if n.op == "call_module"]
+    assert not any(isinstance(c, (torch.nn.BatchNorm2d, torch.nn.ReLU, torch.nn.MaxPool2d)) for c in called)
+    assert sum(isinstance(c, torch.nn.Conv2d) for c in called) == 20
+
+
+def test_no_cpu_fallback():
+    from paper_1804_08378_b200 import frontend as fe
+    gm = fe.optimize(torchvision.models.alexnet().eval())
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        gm(torch.zeros(1, 3, 224, 224))
+
+
+def test_training_model_rejected():
+    from paper_1804_08378_b200 import frontend as fe
+    with pytest.raises(ValueError):
+        fe.optimize(torchvision.models.alexnet().train())
+
+
+def _randomise_bn(m, seed):
+    g = torch.Generator().manual_seed(seed)
+    for mod in m.modules():
+        if isinstance(mod, torch.nn.BatchNorm2d):
+            C = mod.num_features
+            mod.running_mean.copy_(torch.rand(C, generator=g) - 0.5)
+            mod.running_var.copy_(torch.rand(C, generator=g) + 0.5)
+            mod.weight.data.copy_(torch.rand(C, generator=g) + 0.5)
+            mod.bias.data.copy_(torch.rand(C, generator=g) - 0.5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("net", ["alexnet", "vgg11_bn", "resnet18", "resnet50", "densenet121"])
+def test_optimized_network_matches_eager(net, cuda_dev):
+    """The paper's claim at network level: the optimized network computes the same result
+    (P:L72-73).  Convolutions run in cuDNN in both; the stacks run in libbrainslug.so."""
+    from paper_1804_08378_b200 import frontend as fe
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.deterministic = True
+    torch.manual_seed(0)
+    m = getattr(torchvision.models, net)().eval()
+    _randomise_bn(m, 1)
+    m = m.cuda()
+    x = torch.randn(2, 3, 224, 224, device="cuda")
+    with torch.no_grad():
+        ref = m(x)
+        gm = fe.optimize(m)
+        got = gm(x)
+    torch.cuda.synchronize()
+    n_stacks = sum(isinstance(mod, fe.BrainSlugStack) for mod in gm.modules())
+    assert n_stacks == fe.summary(getattr(torchvision.models, net)().eval())["stacks"]
+    assert got.shape == ref.shape
+    scale = ref.abs().max().item()
+    assert torch.allclose(got, ref, rtol=1e-4, atol=1e-4 * max(1.0, scale)), (got - ref).abs().max().item()

@@ -56,7 +56,8 @@ def test_baseline_configs_reduced_batch(wl, cuda_dev, oracle_lib):
         cases = cases[:3] + cases[3:-1:9] + cases[-2:]
     for case in cases:
         x = synth.uniform_np(case.input_seed, int(np.prod(case.shape))).reshape(case.shape)
-        compare(case.layers, x, ctx=case.name)
+        ops = [synth.uniform_np(sd, int(np.prod(case.shape))).reshape(case.shape) for sd in case.operand_seeds]
+        compare(case.layers, x, ops, ctx=case.name)
 
 
 def test_c1_full(cuda_dev, oracle_lib):
@@ -66,25 +67,26 @@ def test_c1_full(cuda_dev, oracle_lib):
     assert got.shape == (1, 16, 16, 16)
 
 
-@pytest.mark.parametrize("wl", ["alexnet", "vgg16", "resnet50", "densenet121"])
+@pytest.mark.parametrize("wl", ["alexnet", "vgg16", "resnet50", "densenet121", "resnet50_residual"])
 def test_full_size_sampled(wl, cuda_dev, oracle_lib):
     """BASELINE.json batch sizes in the launch configuration bench.py times; the oracle
     checks sampled images (every image is an independent unit of the stack)."""
     bs = _bs()
     cases = synth.workload(wl)
     pick = {"alexnet": [0, 1, 2], "vgg16": [0, 2], "resnet50": [0, 1, 7],
-            "densenet121": [0, 1, 60, 119, 120]}[wl]
+            "densenet121": [0, 1, 60, 119, 120], "resnet50_residual": [0, 1, 2, 3]}[wl]
     for idx in pick:
         case = cases[idx]
         N = case.shape[0]
         x = synth.uniform_torch(case.input_seed, case.shape, device="cuda")
+        ops = [synth.uniform_torch(sd, case.shape, device="cuda") for sd in case.operand_seeds]
         plan = bs.bs_plan_create(case.layers, case.shape)
         out = torch.empty(bs.bs_plan_query(plan)["out"], device="cuda")
-        bs.bs_execute(plan, x, out)
+        bs.bs_execute_ex(plan, [x] + ops, out)
         torch.cuda.synchronize()
         for n in sorted({0, N // 2, N - 1}):
             xs = x[n:n + 1].cpu().numpy()
-            ref = oracle.run_bf(case.layers, xs)
+            ref = oracle.run_bf(case.layers, xs, [o[n:n + 1].cpu().numpy() for o in ops])
             U.check(out[n:n + 1].cpu().numpy(), ref, case.layers, f"{case.name} image {n}")
         assert torch.isfinite(out).all()
         del x, out

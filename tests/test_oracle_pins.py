@@ -121,7 +121,8 @@ def test_bc_configs_small_vs_torch(oracle_lib):
                     L = synth.batchnorm(shape[1], case.input_seed)
                 layers.append(L)
             x = synth.uniform_np(case.input_seed, int(np.prod(shape))).reshape(shape)
-            U.check(oracle.run_bf(layers, x), _torch_stack(layers, x, []), layers, case.name)
+            ops = [synth.uniform_np(sd, int(np.prod(shape))).reshape(shape) for sd in case.operand_seeds]
+            U.check(oracle.run_bf(layers, x, ops), _torch_stack(layers, x, ops), layers, case.name)
 
 
 # ----------------------------------------------------------------------------- BN special cases
