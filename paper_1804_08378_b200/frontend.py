@@ -210,9 +210,15 @@ class BrainSlugStack(nn.Module):
         if not x.is_cuda:
             raise RuntimeError(f"BrainSlugStack {self.name}: input on {x.device}; the stack runs only on "
                                "CUDA (sm_100a kernels) -- there is no CPU fallback")
-        if x.dtype != torch.float32 or x.dim() != 4:
+        flat = x.dim() != 4 and all(L.kind in ("relu", "copy", "scale", "add") for L in self.layers)
+        if x.dtype != torch.float32 or not (x.dim() == 4 or flat):
             raise RuntimeError(f"BrainSlugStack {self.name}: needs a 4-D float32 NCHW tensor, got "
                                f"{x.dtype} {tuple(x.shape)}")
+        if flat:   # element-wise stack on a non-image tensor (e.g. a classifier's ReLU/Dropout)
+            shape = x.shape
+            y = self.forward(x.reshape(1, 1, 1, x.numel()),
+                             *[o.expand(shape).reshape(1, 1, 1, x.numel()) for o in operands])
+            return y.reshape(shape)
         x = x.contiguous()
         ops = [o.contiguous() for o in operands]
         key = (tuple(x.shape), x.device.index)
