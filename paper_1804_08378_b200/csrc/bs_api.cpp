@@ -708,6 +708,7 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       a.n_tiles = (a.n_planes + l.tile_planes - 1) / l.tile_planes;
       a.work_floats = l.seq_work_floats;
       a.in_plane = (int32_t)(s.in.h * s.in.w);
+      a.cdiv = make_fastdiv((uint32_t)a.C);
       const int grid = (int)std::min<int64_t>(a.n_tiles, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
       e = launch_seq(a, grid, st);
     } else if (l.kernel == K_EW) {
@@ -948,6 +949,9 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
           }
           d.pro = make_prog(p, st.pro);
           d.epi = make_prog(p, st.epi);
+          d.epi_class = prog_class(st.epi);
+          d.fast = st.has_pool && st.is_max && st.kh == 3 && st.kw == 3 && st.sh == 1 && st.sw == 1 &&
+                   st.ph == 1 && st.pw == 1 && st.pro.empty() && d.epi_class != PC_GENERIC;
           desc.push_back(d);
         }
       }

@@ -237,6 +237,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Explicit shared-memory accesses on 32-bit shared addresses: pointers chosen at run time among
+// several smem buffers otherwise fall back to generic LD/ST (slower, 64-bit addressing).
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));   // ordered by the volatile barriers
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+
+// The same wait with a suspend-time hint: the waiting thread sleeps until the phase completes
+// (or the hint expires) instead of spinning on try_wait -- a producer or an idle consumer warp
+// then takes no issue slots from the warps doing the work.
+#ifndef BS_MBAR_SLEEP_NS
+#define BS_MBAR_SLEEP_NS 0x989680
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(BS_MBAR_SLEEP_NS)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),

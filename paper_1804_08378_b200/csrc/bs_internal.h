@@ -93,6 +93,8 @@ struct SeqStepDev {
   int32_t H, W, Ho, Wo;
   int32_t kh, kw, sh, sw, ph, pw;
   int32_t is_max, count_include_pad;
+  int32_t fast;             // 1: 3x3/s1/p1 max pool, no prologue, epilogue class <= PC_AFFINE_RELU
+  int32_t epi_class;        // ProgClass of epi
   OpProgram pro, epi;
 };
 struct SeqArgs {
@@ -106,6 +108,7 @@ struct SeqArgs {
   int64_t n_tiles;
   int32_t work_floats;      // floats per work buffer (tile_planes x largest intermediate plane)
   int32_t in_plane;         // H0 * W0
+  FastDiv cdiv;             // channels C (plane -> channel)
 };
 cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st);
 size_t seq_smem(const SeqArgs& a);

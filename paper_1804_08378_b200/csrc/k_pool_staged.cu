@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
       int s = 0;
       uint32_t ph = 0;
       for (int k = 0; k < my_tiles; ++k) {
-        if (k >= S) mbar_wait(&empty[s], ph ^ 1);
+        if (k >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
         const int64_t p0 = pb + (int64_t)k * P;
         const int np = (int)min((int64_t)P, pe - p0);
         const float* src = a.in + (a.plane0 + p0) * (int64_t)HW;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
     const int np = (int)min((int64_t)P, pe - p0);
     const float* sm = (const float*)(stage0 + (size_t)s * tile_stride +
                                      ((uintptr_t)(a.in + (a.plane0 + p0) * (int64_t)HW) & 15u));
-    mbar_wait(&full[s], ph);
+    mbar_wait_sleep(&full[s], ph);
 #ifdef BS_DBG_NOCOMPUTE
     if (items < 0)
 #endif

@@ -41,6 +41,92 @@ __device__ __forceinline__ float seq_window(const SeqStepDev& st, const float* p
   return acc;
 }
 
+// Per-step constants of the fast path, hoisted into shared memory once per CTA.
+struct SeqFastStep {
+  int32_t H, W, lg_nb, R;      // plane size; row bands = 1 << lg_nb of R rows
+  int32_t has_aff, has_relu;   // epilogue: folded BN, ReLU
+  const float2* aff;           // (scale, shift) per channel
+};
+
+// One fast step (3x3/s1/p1 max pool + [BN] [ReLU]) over the np planes of a tile: lane owns
+// columns lane and lane + 32 (TWO); a warp walks a band of rows keeping the last two row maxima
+// per column in registers -- 3 LDS per output, immediate offsets off one 32-bit row address.
+// Padding is absent: an edge column replaces its out-of-row neighbour by itself and the bottom
+// row its missing successor (duplicates, exact for max).  LAST: outputs go to HBM.
+template <bool LAST, bool TWO>
+__device__ __forceinline__ void seq_fast_step(const SeqFastStep& f, uint32_t in_s, uint32_t out_s, float* gout,
+                                              int np, uint32_t plane_base, const FastDiv& cdiv, int C, int cw,
+                                              int lane) {
+  const int W = f.W, H = f.H, HW = W * H, R = f.R, lg = f.lg_nb;
+  const uint32_t W4 = 4u * (uint32_t)W;
+  const int j0 = min(lane, W - 1), j1 = min(lane + 32, W - 1);
+  const bool act0 = lane < W, act1 = TWO && lane + 32 < W;
+  const bool l0 = j0 == 0, r0 = j0 == W - 1, r1 = j1 == W - 1;
+  const uint32_t c0off = 4u * (uint32_t)j0, c1off = 4u * (uint32_t)j1;
+  const int items = np << lg;
+  for (int it = cw; it < items; it += kStagedConsumerWarps) {
+    const int p = it >> lg;
+    const int i0 = (it & ((1 << lg) - 1)) * R, i1 = min(H, i0 + R);
+    if (i0 >= i1) continue;
+    const uint32_t plane = plane_base + (uint32_t)p;
+    const int ch = (int)(plane - fdiv(plane, cdiv) * (uint32_t)C);
+    float2 aff = make_float2(1.f, 0.f);
+    if (f.has_aff) aff = __ldg(f.aff + ch);
+    auto epi = [&](float r) -> float {
+      if (f.has_aff) r = __fmaf_rn(r, aff.x, aff.y);
+      if (f.has_relu) r = relu(r);
+      return r;
+    };
+    auto rm0 = [&](uint32_t q) -> float {
+      const float c = lds_f32(q + c0off);
+      const float l = l0 ? c : lds_f32(q + c0off - 4u);
+      const float r = r0 ? c : lds_f32(q + c0off + 4u);
+      return fmaxf(fmaxf(l, c), r);
+    };
+    auto rm1 = [&](uint32_t q) -> float {   // column j1 >= 32: never a left edge
+      const float c = lds_f32(q + c1off);
+      const float l = lds_f32(q + c1off - 4u);
+      const float r = r1 ? c : lds_f32(q + c1off + 4u);
+      return fmaxf(fmaxf(l, c), r);
+    };
+    uint32_t q = in_s + 4u * (uint32_t)(p * HW + i0 * W);
+    const uint32_t qp = i0 > 0 ? q - W4 : q;
+    float a0 = rm0(qp), b0 = rm0(q), a1 = 0.f, b1 = 0.f;
+    if (TWO) { a1 = rm1(qp); b1 = rm1(q); }
+    const int i_end = min(i1, H - 1);   // rows whose successor row exists
+    uint32_t o = out_s + 4u * (uint32_t)(p * HW + i0 * W);
+    float* og = LAST ? gout + (size_t)p * HW + i0 * W : nullptr;
+    auto put = [&](float v0, float v1) {
+      if (LAST) {
+        if (act0) __stcs(og + j0, v0);
+        if (TWO && act1) __stcs(og + j1, v1);
+        og += W;
+      } else {
+        if (act0) sts_f32(o + c0off, v0);
+        if (TWO && act1) sts_f32(o + c1off, v1);
+        o += W4;
+      }
+    };
+#pragma unroll 2
+    for (int i = i0; i < i_end; ++i) {
+      q += W4;
+      const float c0 = rm0(q);
+      const float v0 = epi(fmaxf(fmaxf(a0, b0), c0));
+      a0 = b0;
+      b0 = c0;
+      float v1 = 0.f;
+      if (TWO) {
+        const float c1 = rm1(q);
+        v1 = epi(fmaxf(fmaxf(a1, b1), c1));
+        a1 = b1;
+        b1 = c1;
+      }
+      put(v0, v1);
+    }
+    if (i1 == H) put(epi(fmaxf(a0, b0)), epi(fmaxf(a1, b1)));
+  }
+}
+
 __global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
@@ -69,7 +155,7 @@ __global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
       int k = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
         const int s = k % a.stages;
-        if (k >= a.stages) mbar_wait(&empty[s], ((k / a.stages) - 1) & 1);
+        if (k >= a.stages) mbar_wait_sleep(&empty[s], ((k / a.stages) - 1) & 1);
         const int64_t pl0 = (int64_t)t * a.tile_planes;
         const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
         const float* src = a.in + (a.plane0 + pl0) * (int64_t)HW0;
@@ -94,10 +180,27 @@ __global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
   }
 
   const int cw = warp - 1;   // consumer warp 0..7
+  // per-step constants of the fast path (W = 0: generic step), filled once by warp 1
+  __shared__ SeqFastStep fast_tab[kMaxSeqSteps];
+  if (cw == 0 && lane < a.n_steps) {
+    const SeqStepDev& st = a.steps[lane];
+    SeqFastStep f;
+    f.W = (st.fast && st.W <= 64) ? st.W : 0;
+    f.H = st.H;
+    int lg = 0;   // row bands: a power of two, >= 16 items per tile
+    while ((2 << lg) <= st.H && (a.tile_planes << lg) < 2 * kStagedConsumerWarps) ++lg;
+    f.lg_nb = lg;
+    f.R = (st.H + (1 << lg) - 1) >> lg;
+    f.has_aff = st.epi_class == PC_AFFINE || st.epi_class == PC_AFFINE_RELU;
+    f.has_relu = st.epi_class == PC_RELU || st.epi_class == PC_AFFINE_RELU;
+    f.aff = st.epi.affine[0];
+    fast_tab[lane] = f;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kStagedConsumerWarps) : "memory");
   int k = 0;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
     const int s = k % a.stages;
-    mbar_wait(&full[s], (k / a.stages) & 1);
+    mbar_wait_sleep(&full[s], (k / a.stages) & 1);
     const int64_t pl0 = (int64_t)t * a.tile_planes;
     const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
     const float* src_base = (const float*)((const char*)stage0 + (size_t)s * tile_stride +
@@ -108,6 +211,22 @@ __global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
       const float* in_buf = st_i == 0 ? src_base : work[(st_i - 1) & 1];
       float* out_buf = work[st_i & 1];
       const int HWi = st.H * st.W, HWo = st.Ho * st.Wo;
+      if (fast_tab[st_i].W > 0) {
+        const SeqFastStep& f = fast_tab[st_i];
+        const uint32_t in_s = smem_u32(in_buf), out_s = smem_u32(out_buf);
+        float* gout = a.out + (a.plane0 + pl0) * (int64_t)HWo;
+        const uint32_t pbase = (uint32_t)(a.plane0 + pl0);
+        if (last) {
+          if (f.W > 32) seq_fast_step<true, true>(f, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
+          else seq_fast_step<true, false>(f, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
+        } else {
+          if (f.W > 32) seq_fast_step<false, true>(f, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
+          else seq_fast_step<false, false>(f, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kStagedConsumerWarps) : "memory");   // step boundary
+        if (st_i == 0 && cw == 0 && lane == 0) mbar_arrive(&empty[s]);   // stage buffer consumed
+        continue;
+      }
       // work items: (plane, output row, 32-column chunk); lane = output column
       const int nchunk = (st.Wo + 31) / 32;
       const int items = np * st.Ho * nchunk;

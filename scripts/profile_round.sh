@@ -15,5 +15,6 @@ for spec in "alexnet 0 staged" "alexnet 1 staged" "alexnet 2 staged" "vgg16 0 po
   $NCU -i $rep.ncu-rep --page raw --csv > gpurun_out/prof/full_$1_$2.raw.csv 2>/dev/null
   $NCU -i $rep.ncu-rep --page details --csv > gpurun_out/prof/full_$1_$2.details.csv 2>/dev/null
 done
+$NCU -i /tmp/full_alexnet_0.ncu-rep --page source --csv --print-source sass > gpurun_out/prof/full_alexnet_0.sass.csv 2>/dev/null
 cp /tmp/full_alexnet_0.ncu-rep gpurun_out/prof/ 2>/dev/null
 du -sh gpurun_out

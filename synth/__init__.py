@@ -273,6 +273,17 @@ def workload(name: str, batch: Optional[int] = None) -> List[StackCase]:
     return cases
 
 
+def synthetic51(depth: int, batch: int = 128, C: int = 64, H: int = 56) -> StackCase:
+    """PAPER.md §5.1: a network of `depth` blocks MaxPool3x3/s1/p1 -> BN -> ReLU,
+    every layer optimizable (one stack).  The tensor shape is unstated in the paper (SURVEY.md
+    G20); (128, 64, 56, 56) is DESIGN.md's choice."""
+    cfg = 51
+    layers: List[Layer] = []
+    for b in range(depth):
+        layers += [maxpool(3, 1, 1), batchnorm(C, seed_for(cfg, b, 0)), relu()]
+    return StackCase(f"sec51_depth{depth}", (batch, C, H, H), layers, seed_for(cfg, 9999, 0))
+
+
 WORKLOADS = ("c1", "alexnet", "vgg16", "resnet50", "densenet121", "resnet50_residual")
 DEFAULT_BATCH = {"c1": 1, "alexnet": 128, "vgg16": 64, "resnet50": 256, "densenet121": 256,
                  "resnet50_residual": 256}

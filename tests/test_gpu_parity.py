@@ -222,6 +222,37 @@ def test_sec51_blocks(depth, cuda_dev, oracle_lib):
     U.assert_bitexact(outs[2], outs[0], "unlimited vs 1")
 
 
+@pytest.mark.parametrize("shape", [(2, 3, 56, 56), (2, 2, 33, 45), (1, 2, 1, 1), (1, 1, 7, 64), (3, 5, 2, 31)])
+def test_sec51_fast_path_shapes(shape, cuda_dev, oracle_lib):
+    """The sequence kernel's 3x3/s1/p1 fast path (k_seq.cu) on widths spanning 1-2 column
+    chunks and degenerate planes, under on-chip and 5-step policies."""
+    layers = []
+    for b in range(3):
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(shape[1], 300 + b, signed_gamma=b == 1), synth.relu()]
+    layers += [synth.maxpool(3, 1, 1)]                    # last step: no epilogue
+    x = synth.uniform_np(sum(shape), int(np.prod(shape))).reshape(shape)
+    ref = oracle.run_bf(layers, x)
+    for policy in (0, 5, 2):
+        got, _ = run_gpu(layers, x, opts={"max_steps_per_sequence": policy})
+        U.assert_close(got, ref, f"{shape} policy {policy}")
+
+
+def test_sec51_full_shape_sampled(cuda_dev, oracle_lib):
+    """The §5.1 network at DESIGN.md's benchmark shape (128, 64, 56, 56), depth 16 (one
+    on-chip sequence), images checked against the oracle one by one."""
+    bs = _bs()
+    case = synth.synthetic51(16)
+    x = synth.uniform_torch(case.input_seed, case.shape, device="cuda")
+    plan = bs.bs_plan_create(case.layers, case.shape)
+    assert bs.bs_plan_query(plan)["n_launches"] == 1
+    out = torch.empty(bs.bs_plan_query(plan)["out"], device="cuda")
+    bs.bs_execute(plan, x, out)
+    torch.cuda.synchronize()
+    for n in (0, 77, 127):
+        ref = oracle.run_bf(case.layers, x[n:n + 1].cpu().numpy())
+        U.check(out[n:n + 1].cpu().numpy(), ref, case.layers, f"image {n}")
+
+
 def test_long_elementwise_runs_split(cuda_dev, oracle_lib):
     shape = (2, 3, 9, 11)
     layers = [synth.scale(1.5), synth.relu(), synth.scale(-0.5)] * 6 + [synth.maxpool(2, 2)] + \
