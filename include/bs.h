@@ -148,7 +148,9 @@ typedef struct {
 /*
  * bs_plan_create -- compile phase.
  *   layers/n_layers : the stack, in network order (host memory; copied).
- *   input           : (N, C, H, W) of the stack input; all >= 1.
+ *   input           : (N, C, H, W) of the stack input; C, H, W >= 1.  N = 0 (an empty batch) is
+ *                     valid: the plan reports out.n = 0, 0 launches and 0 algorithmic bytes,
+ *                     and bs_execute* return BS_OK without touching memory (NULL pointers allowed).
  *   opts            : NULL = defaults on the current device.
  *   plan_out        : receives the plan (NULL on failure).
  * Steps performed: validation + shape inference (a1); layer -> op mapping with BN folded

@@ -102,6 +102,7 @@ struct Launch {
 struct bs_plan {
   int device = 0;
   bool host_only = false;
+  bool empty = false;                  // N = 0: geometry planned for N = 1, execute is a no-op
   int num_sms = 148;
   bs_plan_info info{};
   std::vector<Launch> launches;
@@ -771,6 +772,12 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
 bs_status check_exec_args(const bs_plan* p, const float* const* inputs, int32_t n_inputs, const float* out) {
   if (!p) return fail(BS_ERR_INVALID_ARGUMENT, "plan is NULL");
   if (p->host_only) return fail(BS_ERR_INVALID_ARGUMENT, "plan was created host_only; it cannot be executed");
+  if (p->empty) {   // empty batch: nothing is read or written (pointers may be NULL)
+    if (n_inputs != p->info.n_inputs)
+      return fail(BS_ERR_INVALID_ARGUMENT, "plan needs %d inputs (stack input + ADD operands), got %d",
+                  p->info.n_inputs, n_inputs);
+    return BS_OK;
+  }
   if (!inputs || !out) return fail(BS_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
   if (n_inputs != p->info.n_inputs)
     return fail(BS_ERR_INVALID_ARGUMENT, "plan needs %d inputs (stack input + ADD operands), got %d",
@@ -850,6 +857,9 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
   o.device = -1;
   if (opts) o = *opts;
 
+  // an empty batch (N = 0) is valid: plan the geometry of one image, execute nothing
+  const bool empty_batch = input.n == 0;
+  if (empty_batch) input.n = 1;
   std::vector<Shape4> shapes;
   int n_inputs = 1;
   bs_status st = validate_and_shape(layers, n_layers, input, shapes, n_inputs);
@@ -909,6 +919,12 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
     }
   }
   fill_info(p, shapes, n_layers, n_inputs);
+  if (empty_batch) {
+    p->empty = true;
+    p->info.out.n = 0;
+    p->info.alg_bytes_read = p->info.alg_bytes_written = 0;
+    p->info.n_launches = 0;
+  }
   fill_launch_info(p);
 
   if (!p->host_only) {
@@ -1002,7 +1018,7 @@ bs_status bs_plan_query_launch(const bs_plan* plan, int32_t index, bs_launch_inf
 bs_status bs_execute_ex(const bs_plan* plan, const float* const* inputs, int32_t n_inputs, float* out,
                         bs_stream_t stream) {
   bs_status st = check_exec_args(plan, inputs, n_inputs, out);
-  if (st != BS_OK) return st;
+  if (st != BS_OK || plan->empty) return st;
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != plan->device) cudaSetDevice(plan->device);
@@ -1018,9 +1034,9 @@ bs_status bs_execute(const bs_plan* plan, const float* in, float* out, bs_stream
 
 bs_status bs_execute_host(const bs_plan* plan, const float* const* h_inputs, int32_t n_inputs, float* h_out,
                           float* const* d_inputs, float* d_out, int32_t n_chunks, bs_stream_t stream) {
-  if (!h_inputs || !h_out) return fail(BS_ERR_INVALID_ARGUMENT, "NULL host pointer");
   bs_status st = check_exec_args(plan, (const float* const*)d_inputs, n_inputs, d_out);
-  if (st != BS_OK) return st;
+  if (st != BS_OK || plan->empty) return st;
+  if (!h_inputs || !h_out) return fail(BS_ERR_INVALID_ARGUMENT, "NULL host pointer");
   for (int k = 0; k < n_inputs; ++k)
     if (!h_inputs[k]) return fail(BS_ERR_INVALID_ARGUMENT, "h_inputs[%d] is NULL", k);
   const int64_t N = plan->launches.front().step.in.n;

@@ -216,8 +216,8 @@ class BrainSlugStack(nn.Module):
                                f"{x.dtype} {tuple(x.shape)}")
         if flat:   # element-wise stack on a non-image tensor (e.g. a classifier's ReLU/Dropout)
             shape = x.shape
-            y = self.forward(x.reshape(1, 1, 1, x.numel()),
-                             *[o.expand(shape).reshape(1, 1, 1, x.numel()) for o in operands])
+            flat4 = (1, 1, 1, x.numel()) if x.numel() else (0, 1, 1, 1)   # empty: an empty batch
+            y = self.forward(x.reshape(flat4), *[o.expand(shape).reshape(flat4) for o in operands])
             return y.reshape(shape)
         x = x.contiguous()
         ops = [o.contiguous() for o in operands]

@@ -197,3 +197,15 @@ def test_tile_policy_fills_device(bs):
         assert li["n_tasks"] >= 148 * 40
         if li["halo_rows"]:
             assert li["halo_rows"] / (li["rows_per_task"] * li["pool_sh"]) <= 1 / 8 + 1e-9
+
+
+def test_empty_batch_plan(bs):
+    """N = 0 (an empty batch) plans the geometry of one image and reports no work."""
+    p = host_plan(bs, [synth.batchnorm(3, 5), synth.relu(), synth.maxpool(3, 2, 1)], (0, 3, 13, 13))
+    info = bs.bs_plan_query(p)
+    assert info["out"] == (0, 3, 7, 7)
+    assert (info["n_launches"], info["alg_bytes_read"], info["alg_bytes_written"]) == (0, 0, 0)
+    for bad in [(2, 0, 8, 8), (2, 3, 0, 8), (2, 3, 8, 0), (-1, 3, 8, 8)]:
+        with pytest.raises(bs.BsError) as e:
+            host_plan(bs, [synth.relu()], bad)
+        assert e.value.status == 2

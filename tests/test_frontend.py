@@ -96,3 +96,5 @@ def test_optimized_network_matches_eager(net, cuda_dev):
     assert got.shape == ref.shape
     scale = ref.abs().max().item()
     assert torch.allclose(got, ref, rtol=1e-4, atol=1e-4 * max(1.0, scale)), (got - ref).abs().max().item()
+    with torch.no_grad():   # an empty batch goes through every stack as a no-op
+        assert gm(x[:0]).shape == (0,) + tuple(ref.shape[1:])

@@ -331,6 +331,21 @@ def test_argument_errors(cuda_dev):
     torch.cuda.synchronize()
 
 
+def test_empty_batch(cuda_dev):
+    """An empty batch executes as a no-op through every entry point (NULL pointers allowed)."""
+    bs = _bs()
+    for layers in ([synth.relu(), synth.maxpool(3, 2)], [synth.batchnorm(4, 9), synth.add(1), synth.relu()]):
+        plan = bs.bs_plan_create(layers, (0, 4, 13, 13))
+        n_in = bs.bs_plan_query(plan)["n_inputs"]
+        x = torch.empty((0, 4, 13, 13), device="cuda")
+        out = torch.empty(bs.bs_plan_query(plan)["out"], device="cuda")
+        bs.bs_execute_ex(plan, [x] * n_in, out)
+        bs.bs_execute_ex(plan, [0] * n_in, 0)
+        bs.bs_execute_host(plan, [0] * n_in, 0, [0] * n_in, 0)
+        torch.cuda.synchronize()
+        assert out.shape[0] == 0
+
+
 def test_ew_large_tensor_rebasing(cuda_dev, oracle_lib):
     """> 2^31 elements: the element-wise launcher splits at 4-image boundaries."""
     bs = _bs()
