@@ -750,17 +750,9 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       a.out = dst;
       a.plane0 = img0 * s.in.c;
       a.n_planes = (img1 - img0) * s.in.c;
-      Launch lk = l;
-      if (false) {
-        // sub-range not 16-B aligned for the bulk copy: global-memory walker
-        set_spec_geometry(lk, 0);
-        a.G = lk.G; a.gw = lk.gw; a.Jg = lk.Jg; a.n_cc = lk.n_cc;
-        a.rows_per_task = lk.rows_per_task; a.n_rb = lk.n_rb;
-      }
-      const int kind = lk.kernel;
-      a.n_tasks = pool_tasks(lk, a.n_planes);
+      a.n_tasks = pool_tasks(l, a.n_planes);
       a.n_tiles = a.n_tasks;
-      e = launch_pool(a, kind, pool_grid(p, lk, a.n_tasks), 256, st);
+      e = launch_pool(a, l.kernel, pool_grid(p, l, a.n_tasks), 256, st);
     }
     if (e != cudaSuccess)
       return fail(BS_ERR_CUDA, "launch %zu (layers %d..%d): %s", k, s.first_layer, s.last_layer,
