@@ -209,6 +209,26 @@ BS_API bs_status bs_execute_host(const bs_plan *plan, const float *const *h_inpu
  * must ensure no execution using the plan is still in flight. */
 BS_API void bs_plan_destroy(bs_plan *plan);
 
+/*
+ * bs_graph_* -- a whole network's stacks as ONE CUDA graph ("a CUDA
+ * graph over all of a network's stacks"; small stacks are launch-bound).  The
+ * launches of n_plans executions -- plans[i] on inputs[i][0..n_inputs_i) -> outs[i], in array
+ * order, each ordered after the previous one exactly as consecutive bs_execute_ex calls on
+ * one stream -- are captured once and replayed by bs_graph_launch with a single host call.
+ *   plans / inputs / outs : as bs_execute_ex, per execution; n_inputs[i] = the plan's n_inputs.
+ *                           Device pointers are BOUND at creation (graph semantics): a replay
+ *                           reads and writes the same buffers.  All plans on one device.
+ *   graph_out             : receives the graph.  Errors: as bs_execute_ex (index named), and
+ *                           BS_ERR_CUDA if capture or instantiation fails.
+ * Ownership: the graph references the plans (their parameters / intermediates); destroy the
+ * graph before any of its plans.  Replays on one stream are ordered like any kernel launch.
+ */
+typedef struct bs_graph bs_graph;
+BS_API bs_status bs_graph_create(const bs_plan *const *plans, int32_t n_plans, const float *const *const *inputs,
+                                 const int32_t *n_inputs, float *const *outs, bs_graph **graph_out);
+BS_API bs_status bs_graph_launch(const bs_graph *graph, bs_stream_t stream);
+BS_API void bs_graph_destroy(bs_graph *graph);   /* NULL-safe; no replay may be in flight */
+
 /* Thread-local description of the last error on this thread ("" if none). */
 BS_API const char *bs_last_error(void);
 

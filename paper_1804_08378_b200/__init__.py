@@ -92,6 +92,13 @@ _lib.bs_execute.argtypes = [_P, _P, _P, _P]
 _lib.bs_execute_ex.argtypes = [_P, ctypes.POINTER(_P), ctypes.c_int32, _P, _P]
 _lib.bs_execute_host.argtypes = [_P, ctypes.POINTER(_P), ctypes.c_int32, _P, ctypes.POINTER(_P), _P,
                                  ctypes.c_int32, _P]
+_lib.bs_graph_create.argtypes = [ctypes.POINTER(_P), ctypes.c_int32, ctypes.POINTER(ctypes.POINTER(_P)),
+                                 ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_P), ctypes.POINTER(_P)]
+_lib.bs_graph_create.restype = ctypes.c_int
+_lib.bs_graph_launch.argtypes = [_P, _P]
+_lib.bs_graph_launch.restype = ctypes.c_int
+_lib.bs_graph_destroy.argtypes = [_P]
+_lib.bs_graph_destroy.restype = None
 _lib.bs_plan_destroy.argtypes = [_P]
 _lib.bs_plan_destroy.restype = None
 _lib.bs_last_error.restype = ctypes.c_char_p
@@ -242,6 +249,50 @@ def bs_execute_host(plan: Plan, h_inputs: Sequence, h_out, d_inputs: Sequence, d
 
 def bs_plan_destroy(plan: Plan) -> None:
     plan.close()
+
+
+class Graph:
+    """Owns a bs_graph* (bs_graph_destroy on close/GC); keeps its plans alive."""
+
+    def __init__(self, handle: int, plans):
+        self.handle = handle
+        self._plans = list(plans)
+
+    def close(self):
+        if self.handle:
+            _lib.bs_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def _as_parameter_(self):
+        return _P(self.handle)
+
+
+def bs_graph_create(executions: Sequence) -> Graph:
+    """executions: [(plan, [input, operand, ...], out), ...] -- captured in order as one CUDA graph."""
+    n = len(executions)
+    plans = (_P * n)(*[_P(e[0].handle) for e in executions])
+    arrs = [(_P * len(e[1]))(*[_ptr(t) for t in e[1]]) for e in executions]
+    ins = (ctypes.POINTER(_P) * n)(*[ctypes.cast(a, ctypes.POINTER(_P)) for a in arrs])
+    nin = (ctypes.c_int32 * n)(*[len(e[1]) for e in executions])
+    outs = (_P * n)(*[_ptr(e[2]) for e in executions])
+    h = _P()
+    _check(_lib.bs_graph_create(plans, n, ins, nin, outs, ctypes.byref(h)), "bs_graph_create")
+    return Graph(h.value, [e[0] for e in executions])
+
+
+def bs_graph_launch(graph: Graph, stream=None) -> None:
+    _check(_lib.bs_graph_launch(graph, _stream(stream)), "bs_graph_launch")
+
+
+def bs_graph_destroy(graph: Graph) -> None:
+    graph.close()
 
 
 def bs_last_error() -> str:

@@ -1086,4 +1086,76 @@ bs_status bs_execute_host(const bs_plan* plan, const float* const* h_inputs, int
 
 void bs_plan_destroy(bs_plan* plan) { free_plan(plan); }
 
+struct bs_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int device = 0;
+};
+
+bs_status bs_graph_create(const bs_plan* const* plans, int32_t n_plans, const float* const* const* inputs,
+                          const int32_t* n_inputs, float* const* outs, bs_graph** graph_out) {
+  g_err.clear();
+  if (!graph_out) return fail(BS_ERR_INVALID_ARGUMENT, "graph_out is NULL");
+  *graph_out = nullptr;
+  if (!plans || !inputs || !n_inputs || !outs || n_plans < 1)
+    return fail(BS_ERR_INVALID_ARGUMENT, "NULL array or n_plans < 1 (%d)", n_plans);
+  for (int32_t i = 0; i < n_plans; ++i) {
+    bs_status st = check_exec_args(plans[i], inputs[i], n_inputs[i], outs[i]);
+    if (st != BS_OK) return fail(st, "execution %d: %s", i, g_err.c_str());
+    if (plans[i]->device != plans[0]->device)
+      return fail(BS_ERR_INVALID_ARGUMENT, "execution %d: plan on device %d, execution 0 on device %d", i,
+                  plans[i]->device, plans[0]->device);
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  const int dev = plans[0]->device;
+  if (prev != dev) cudaSetDevice(dev);
+  bs_graph* g = new (std::nothrow) bs_graph();
+  if (!g) {
+    if (prev != dev) cudaSetDevice(prev);
+    return fail(BS_ERR_OUT_OF_MEMORY, "host allocation failed");
+  }
+  g->device = dev;
+  cudaStream_t cs = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  bs_status st = BS_OK;
+  if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    for (int32_t i = 0; i < n_plans && st == BS_OK; ++i)
+      if (!plans[i]->empty) st = enqueue(plans[i], inputs[i], outs[i], 0, plans[i]->launches.front().step.in.n, cs);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(cs, &graph);   // always end the capture
+    g->graph = graph;
+    if (e2 != cudaSuccess && st == BS_OK) e = e2;
+  }
+  if (e == cudaSuccess && st == BS_OK) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (cs) cudaStreamDestroy(cs);
+  if (prev != dev) cudaSetDevice(prev);
+  if (st != BS_OK || e != cudaSuccess) {
+    bs_graph_destroy(g);
+    if (st != BS_OK) return st;
+    return fail(BS_ERR_CUDA, "bs_graph_create: %s", cudaGetErrorString(e));
+  }
+  *graph_out = g;
+  return BS_OK;
+}
+
+bs_status bs_graph_launch(const bs_graph* g, bs_stream_t stream) {
+  if (!g || !g->exec) return fail(BS_ERR_INVALID_ARGUMENT, "graph is NULL");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != g->device) cudaSetDevice(g->device);
+  cudaError_t e = cudaGraphLaunch(g->exec, (cudaStream_t)stream);
+  if (prev != g->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(BS_ERR_CUDA, "bs_graph_launch: %s", cudaGetErrorString(e));
+  return BS_OK;
+}
+
+void bs_graph_destroy(bs_graph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+}
+
 }  // extern "C"

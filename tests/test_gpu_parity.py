@@ -331,6 +331,38 @@ def test_argument_errors(cuda_dev):
     torch.cuda.synchronize()
 
 
+def test_graph_matches_sequential_execution(cuda_dev, oracle_lib):
+    """NEXT-3: a CUDA graph over several stacks (incl. an ADD operand, an on-chip sequence, a
+    serialised multi-sequence plan and an empty batch) replays to the oracle's results."""
+    bs = _bs()
+    cases = []
+    for wl, idx in (("alexnet", 0), ("resnet50", 0), ("resnet50_residual", 3), ("densenet121", -1)):
+        c = synth.workload(wl, batch=2)[idx]
+        cases.append((c.layers, c.shape, len(c.operand_seeds)))
+    sec = synth.synthetic51(5, batch=2, C=3, H=17)
+    cases.append((sec.layers, sec.shape, 0))
+    cases.append(([synth.relu(), synth.maxpool(2, 2)], (0, 3, 8, 8), 0))
+    execs, refs, outs = [], [], []
+    for k, (layers, shape, n_ops) in enumerate(cases):
+        opts = {"max_steps_per_sequence": 2} if layers is sec.layers else None
+        plan = bs.bs_plan_create(layers, shape, opts)
+        x = synth.uniform_np(50 + k, int(np.prod(shape))).reshape(shape)
+        ops = [synth.uniform_np(60 + k + j, int(np.prod(shape))).reshape(shape) for j in range(n_ops)]
+        xd = [torch.from_numpy(t).cuda() for t in [x] + ops]
+        out = torch.full(bs.bs_plan_query(plan)["out"], float("nan"), device="cuda")
+        execs.append((plan, xd, out))
+        refs.append((oracle.run_bf(layers, x, ops) if shape[0] else None, layers))
+        outs.append(out)
+    g = bs.bs_graph_create(execs)
+    for _ in range(2):   # replays are idempotent
+        bs.bs_graph_launch(g)
+    torch.cuda.synchronize()
+    for out, (ref, layers) in zip(outs, refs):
+        if ref is not None:
+            U.check(out.cpu().numpy(), ref, layers, "graph replay")
+    bs.bs_graph_destroy(g)
+
+
 def test_empty_batch(cuda_dev):
     """An empty batch executes as a no-op through every entry point (NULL pointers allowed)."""
     bs = _bs()
