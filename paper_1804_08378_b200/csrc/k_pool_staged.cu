@@ -12,9 +12,9 @@ namespace bs {
 // through two smem buffers swapped per step; here whole planes are staged, so
 // overlapping 3x3/s2 windows need no halo re-reads from HBM at all.
 //
-//  * Each persistent CTA owns one contiguous range of planes (n_planes * b / grid ...), cut
-//    into tiles of <= P planes: the CTAs' work differs by at most one plane, whatever the tile
-//    size, and each CTA streams one contiguous region of HBM.
+//  * Persistent CTAs take tiles of P planes round-robin (tile b, b + grid, ...), so the grid
+//    streams one advancing window of HBM (-DBS_STAGED_CONTIGUOUS: one contiguous plane range
+//    per CTA instead, balanced to one plane but ~2 % slower on B200).
 //  * All 8 consumer warps work on the same tile at once: the tile's I items -- (group of G
 //    planes, column chunk, band of R output rows) -- are dealt to the warps in a fixed
 //    pattern (item w, w+8, ...), the planner choosing P and R so that I is a multiple of 8.
@@ -45,9 +45,20 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = a.tile_planes, S = a.stages;
   // this CTA's contiguous plane range [pb, pe)
+#ifndef BS_STAGED_CONTIGUOUS
+  // tiles dealt round-robin (CTA b takes tiles b, b + grid, ...): at any moment the CTAs stream
+  // one contiguous window of HBM, measured 1.5-2.5 % faster on the AlexNet stacks than one
+  // contiguous plane range per CTA (-DBS_STAGED_CONTIGUOUS)
+  const int64_t n_tiles_all = (a.n_planes + P - 1) / P;
+  const int my_tiles = (int)((n_tiles_all - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const int64_t pe = a.n_planes;
+#define BS_TILE_P0(k) ((int64_t)(blockIdx.x + (int64_t)(k) * gridDim.x) * P)
+#else
   const int64_t pb = a.n_planes * (int64_t)blockIdx.x / gridDim.x;
   const int64_t pe = a.n_planes * ((int64_t)blockIdx.x + 1) / gridDim.x;
   const int my_tiles = (int)((pe - pb + P - 1) / P);
+#define BS_TILE_P0(k) (pb + (int64_t)(k) * P)
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -67,7 +78,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
       uint32_t ph = 0;
       for (int k = 0; k < my_tiles; ++k) {
         if (k >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
-        const int64_t p0 = pb + (int64_t)k * P;
+        const int64_t p0 = BS_TILE_P0(k);
         const int np = (int)min((int64_t)P, pe - p0);
         const float* src = a.in + (a.plane0 + p0) * (int64_t)HW;
         const uint32_t head_off = (uint32_t)((uintptr_t)src & 15u);
@@ -123,7 +134,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   int s = 0;
   uint32_t ph = 0;
   for (int k = 0; k < my_tiles; ++k) {
-    const int64_t p0 = pb + (int64_t)k * P;
+    const int64_t p0 = BS_TILE_P0(k);
     const int np = (int)min((int64_t)P, pe - p0);
     const float* sm = (const float*)(stage0 + (size_t)s * tile_stride +
                                      ((uintptr_t)(a.in + (a.plane0 + p0) * (int64_t)HW) & 15u));
