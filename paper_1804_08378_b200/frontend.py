@@ -84,6 +84,10 @@ def _classify(gm: fx.GraphModule, n: fx.Node) -> Optional[Tuple[LayerSpec, fx.No
                 return None
             return LayerSpec("batchnorm", eps=float(m.eps), module=m), x, None
         if isinstance(m, nn.ReLU):
+            # an in-place ReLU also rewrites its input for that input's other consumers: keep
+            # such a node in eager PyTorch (a stack writes a new tensor)
+            if m.inplace and len(x.users) > 1:
+                return None
             return LayerSpec("relu"), x, None
         if isinstance(m, nn.MaxPool2d):
             if _pair(m.dilation) != (1, 1) or m.ceil_mode or m.return_indices:
@@ -105,6 +109,8 @@ def _classify(gm: fx.GraphModule, n: fx.Node) -> Optional[Tuple[LayerSpec, fx.No
         return None
     if n.op == "call_function":
         if n.target in (F.relu, torch.relu) and n.args and isinstance(n.args[0], fx.Node):
+            if n.kwargs.get("inplace", False) and len(n.args[0].users) > 1:
+                return None
             return LayerSpec("relu"), n.args[0], None
         if n.target is F.adaptive_avg_pool2d and len(n.args) >= 2 and isinstance(n.args[0], fx.Node) \
                 and _is_global(n.args[1]):

@@ -48,6 +48,26 @@ def test_optimized_graph_structure():
     assert sum(isinstance(c, torch.nn.Conv2d) for c in called) == 20
 
 
+def test_inplace_relu_with_other_consumers_stays_eager():
+    """x = conv(x); y = relu_(x); z = x + 1 -- the in-place ReLU changes x for z too, so it must
+    not become a stack (which would write a new tensor)."""
+    from paper_1804_08378_b200 import frontend as fe
+
+    class M(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.conv = torch.nn.Conv2d(3, 3, 1)
+            self.relu = torch.nn.ReLU(inplace=True)
+
+        def forward(self, x):
+            x = self.conv(x)
+            y = self.relu(x)
+            return y * 2.0 + x
+
+    d = fe.summary(M().eval())
+    assert d["signatures"] == ["[scale,add]"]   # the ReLU stays in PyTorch
+
+
 def test_no_cpu_fallback():
     from paper_1804_08378_b200 import frontend as fe
     gm = fe.optimize(torchvision.models.alexnet().eval())
