@@ -209,3 +209,17 @@ def test_empty_batch_plan(bs):
         with pytest.raises(bs.BsError) as e:
             host_plan(bs, [synth.relu()], bad)
         assert e.value.status == 2
+
+
+def test_graph_argument_errors(bs):
+    """bs_graph_create validates every execution like bs_execute_ex (no GPU needed to fail)."""
+    import ctypes
+    p = host_plan(bs, [synth.relu()], (1, 2, 4, 4))
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_graph_create([(p, [0], 0)])                       # host_only plan
+    assert e.value.status == 2 and "execution 0" in str(e.value)
+    h = ctypes.c_void_p()
+    st = bs._lib.bs_graph_create(None, 0, None, None, None, ctypes.byref(h))
+    assert st == 2 and not h.value
+    assert bs._lib.bs_graph_launch(None, None) == 2
+    bs._lib.bs_graph_destroy(None)                              # NULL-safe
