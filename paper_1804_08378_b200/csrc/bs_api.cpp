@@ -15,6 +15,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <string>
 #include <vector>
@@ -87,6 +88,7 @@ struct Launch {
   // pool geometry (kernels 2/3)
   int32_t G = 1, gw = 32, Jg = 1, n_cc = 1, rows_per_task = 1, n_rb = 1, U = 1;
   int32_t tile_planes = 0, stages = 0;   // staged kernel
+  int32_t ctas_per_sm = 0;               // staged kernel: CTAs per SM the grid is sized for (0 = occupancy)
   int32_t block = 256;
   int32_t blocks_per_sm = 0;
   bool deferred = false;            // max pool: monotone prologue moved after the pool
@@ -307,7 +309,6 @@ void set_device_programs(Launch& l) {
 // barrier work).  Ring depth: as many stages as fit two CTAs per SM (<= 8).  False if one
 // plane group is too large to stage.
 constexpr int64_t kStagedTileMax = 32 * 1024;
-constexpr int64_t kStagedSmemPerCta = 110 * 1024;   // two CTAs per SM
 bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_sms) {
   const Step& st = l.step;
   const int64_t HW = st.in.h * st.in.w, Ho = st.out.h;
@@ -337,14 +338,22 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
     }
   }
   const int64_t stride = (int64_t)pool_staged_stride((int)bP, (int)HW);
-  const int64_t obufs = 0;
   if (stride > 100 * 1024) return false;   // plane group too large to stage
   l.tile_planes = (int32_t)bP;
   l.rows_per_task = (int32_t)bR;
   l.n_rb = (int32_t)((Ho + bR - 1) / bR);
-  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kStagedMaxStages, (kStagedSmemPerCta - obufs) / stride));
+  // Ring depth: ~104 KB of tiles in flight per SM.  Measured on B200 (AlexNet stacks, CTAs/SM x
+  // stages swept): more bytes in flight is *slower* (2 CTAs x 4 x 24 KB: 22.5 us; 1 CTA x 4-5 x
+  // 24 KB: 20.5 us on s1), so one CTA per SM for tiles >= 20 KB when each SM has >= 12 tiles,
+  // two (more consumer warps per byte) otherwise (s3, 13.5 KB tiles: 2 x 4 stages 6.1 us vs
+  // 1 x 7 stages 6.5 us; DenseNet final, 31 KB tiles, 11 per SM: 2 CTAs).
+  constexpr int64_t kInflightPerSm = 104 * 1024;
+  const int64_t tiles_per_sm = (n_planes + bP - 1) / bP / std::max(1, num_sms);
+  l.ctas_per_sm = (stride >= 20 * 1024 && tiles_per_sm >= 12) ? 1 : 2;   // short kernels: more consumers
+  l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kStagedMaxStages,
+                                                            (kInflightPerSm / l.ctas_per_sm + stride / 2) / stride));
   if (o.force_stages >= 2) l.stages = std::min(kStagedMaxStages, o.force_stages);
-  if ((int64_t)l.stages * stride + obufs > 220 * 1024) l.stages = (int32_t)((220 * 1024 - obufs) / stride);
+  if ((int64_t)l.stages * stride > 220 * 1024) l.stages = (int32_t)((220 * 1024) / stride);
   if (l.stages < 2) return false;
   l.U = 1;
   return true;
@@ -910,6 +919,7 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
         bps = pool_max_blocks_per_sm(l.kernel, probe, 256);
       }
       l.blocks_per_sm = bps > 0 ? bps : 5;
+      if (l.kernel == K_POOL_STAGED && l.ctas_per_sm > 0) l.blocks_per_sm = std::min(l.blocks_per_sm, l.ctas_per_sm);
       if (l.kernel != K_POOL_NAIVE && l.kernel != K_POOL_STAGED) size_rows(p, l, o, l.step.in.n * l.step.in.c);
     }
   }
