@@ -223,3 +223,19 @@ def test_graph_argument_errors(bs):
     assert st == 2 and not h.value
     assert bs._lib.bs_graph_launch(None, None) == 2
     bs._lib.bs_graph_destroy(None)                              # NULL-safe
+
+
+def test_staged_ring_policy(bs):
+    """Staged pools: tiles sized so the 8 consumer warps share each tile (<= 16 items), and the
+    grid sized for ~104 KB of tiles in flight per SM -- one CTA per SM for >= 20 KB tiles with
+    >= 12 tiles per SM, two otherwise (measured on B200)."""
+    info = {}
+    for c in synth.workload("alexnet"):
+        p = host_plan(bs, c.layers, c.shape)
+        info[c.name] = bs.bs_plan_query_launch(p, 0)
+    sms = 148
+    assert all(li["kernel"] == 6 for li in info.values())
+    assert info["alexnet_s1"]["grid"] == sms and info["alexnet_s2"]["grid"] == sms      # 24 KB tiles
+    assert info["alexnet_s3"]["grid"] == 2 * sms                                       # 13.5 KB tiles
+    for li in info.values():
+        assert 1 <= li["rows_per_task"] <= li["out"][2]
