@@ -2,7 +2,8 @@
 #include "bs_device.cuh"
 
 #include <mutex>
-#include <unordered_set>
+#include <set>
+#include <utility>
 
 namespace bs {
 
@@ -30,9 +31,11 @@ static void* pool_fn(int kind, const PoolArgs& a) {
 void prefer_max_shared(const void* fn) {
 #ifndef BS_NO_CARVEOUT
   static std::mutex mu;
-  static std::unordered_set<const void*> done;
+  static std::set<std::pair<const void*, int>> done;   // per (kernel, device)
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  if (done.insert(fn).second)
+  if (done.insert({fn, dev}).second)
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
 #else
   (void)fn;
