@@ -349,7 +349,11 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
   // 1 x 7 stages 6.5 us; DenseNet final, 31 KB tiles, 11 per SM: 2 CTAs).
   constexpr int64_t kInflightPerSm = 104 * 1024;
   const int64_t tiles_per_sm = (n_planes + bP - 1) / bP / std::max(1, num_sms);
-  l.ctas_per_sm = (stride >= 20 * 1024 && tiles_per_sm >= 12) ? 1 : 2;   // short kernels: more consumers
+  // one CTA per SM only for big tiles, long kernels and pools that shrink the plane (stride >= 2:
+  // few outputs per staged byte); stride-1 pools (the §5.1 block: one output per input) need the
+  // second CTA's consumer warps (41 vs 47 us per block measured)
+  const bool shrinks = 2 * st.out.h * st.out.w <= HW;
+  l.ctas_per_sm = (stride >= 20 * 1024 && tiles_per_sm >= 12 && shrinks) ? 1 : 2;
   l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kStagedMaxStages,
                                                             (kInflightPerSm / l.ctas_per_sm + stride / 2) / stride));
   if (o.force_stages >= 2) l.stages = std::min(kStagedMaxStages, o.force_stages);
