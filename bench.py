@@ -419,15 +419,15 @@ def main():
     probe = int(min(h2d, 256 << 20))   # (at most 256 MB of pinned memory for the probe)
     hb = torch.empty(probe // 4, dtype=torch.float32).pin_memory()
     db = torch.empty(probe // 4, dtype=torch.float32, device=dev)
-    db.copy_(hb, non_blocking=True)
-    torch.cuda.synchronize()
-    a.record(stream)
+    pcie_gbs = 0.0
     with torch.cuda.stream(stream):
-        for _ in range(3):
+        for r in range(7):   # 2 warm-up copies, then the best of 5
+            a.record(stream)
             db.copy_(hb, non_blocking=True)
-    b.record(stream)
-    torch.cuda.synchronize()
-    pcie_gbs = 3 * probe / (a.elapsed_time(b) / 1e3) / 1e9
+            b.record(stream)
+            torch.cuda.synchronize()
+            if r >= 2:
+                pcie_gbs = max(pcie_gbs, probe / (a.elapsed_time(b) / 1e3) / 1e9)
     del hb, db
     e2e_h2d_gbs = h2d / (e2e_ms / e2e_steps / 1e3) / 1e9
     e2e = {"value": images / (e2e_ms / e2e_steps / 1e3), "unit": "images/s", "h2d_bytes_per_step": int(h2d),
@@ -435,7 +435,7 @@ def main():
            "path": "bs_execute_host: pinned host -> device copy, kernels, device -> host copy, pipelined per chunk",
            "roofline": {"bound": "pcie_h2d", "achieved_gbs": e2e_h2d_gbs, "peak_gbs": pcie_gbs,
                         "frac": e2e_h2d_gbs / pcie_gbs,
-                        "peak_source": "measured: pinned host -> device torch copy of the same bytes"}}
+                        "peak_source": "measured: best of 5 pinned host -> device torch copies of the same bytes (<= 256 MB)"}}
 
     # ---- layer-by-layer torch eager on the same GPU (the paper's comparison system, re-hosted)
     lbl = None
