@@ -675,7 +675,7 @@ void fill_launch_info(bs_plan* p) {
       li.rows_per_task = (int32_t)s.out.h;
       li.n_tasks = (n_planes + l.tile_planes - 1) / l.tile_planes;
       li.grid = (int)std::min<int64_t>(li.n_tasks, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
-      li.block = kStagedThreads;
+      li.block = kSeqThreads;
     } else {
       li.groups_per_warp = l.G;
       li.outputs_per_group = l.Jg;

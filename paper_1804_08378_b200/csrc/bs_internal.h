@@ -132,6 +132,11 @@ int pool_vec_unroll(int vec);
 #endif
 constexpr int kStagedConsumerWarps = BS_STAGED_CW;
 constexpr int kStagedThreads = 32 * (kStagedConsumerWarps + 1);
+#ifndef BS_SEQ_CW
+#define BS_SEQ_CW 8
+#endif
+constexpr int kSeqWarps = BS_SEQ_CW;            // consumer warps of the on-chip sequence kernel
+constexpr int kSeqThreads = 32 * (kSeqWarps + 1);
 constexpr int kStagedMaxStages = 8;    // mbarrier pairs in the staged kernels' smem header
 constexpr int kStagedHeader = 128;     // bytes of smem before the first stage
 size_t pool_staged_smem(int tile_planes, int HW, int HWo, int stages);

@@ -64,7 +64,7 @@ __device__ __forceinline__ void seq_fast_step(const SeqFastStep& f, uint32_t in_
   const bool l0 = j0 == 0, r0 = j0 == W - 1, r1 = j1 == W - 1;
   const uint32_t c0off = 4u * (uint32_t)j0, c1off = 4u * (uint32_t)j1;
   const int items = np << lg;
-  for (int it = cw; it < items; it += kStagedConsumerWarps) {
+  for (int it = cw; it < items; it += kSeqWarps) {
     const int p = it >> lg;
     const int i0 = (it & ((1 << lg) - 1)) * R, i1 = min(H, i0 + R);
     if (i0 >= i1) continue;
@@ -127,7 +127,7 @@ __device__ __forceinline__ void seq_fast_step(const SeqFastStep& f, uint32_t in_
   }
 }
 
-__global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
+__global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
   uint64_t* empty = full + 8;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
     f.W = (st.fast && st.W <= 64) ? st.W : 0;
     f.H = st.H;
     int lg = 0;   // row bands: a power of two, >= 16 items per tile
-    while ((2 << lg) <= st.H && (a.tile_planes << lg) < 2 * kStagedConsumerWarps) ++lg;
+    while ((2 << lg) <= st.H && (a.tile_planes << lg) < 2 * kSeqWarps) ++lg;
     f.lg_nb = lg;
     f.R = (st.H + (1 << lg) - 1) >> lg;
     f.has_aff = st.epi_class == PC_AFFINE || st.epi_class == PC_AFFINE_RELU;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
     f.aff = st.epi.affine[0];
     fast_tab[lane] = f;
   }
-  asm volatile("bar.sync 1, %0;" ::"r"(32 * kStagedConsumerWarps) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kSeqWarps) : "memory");
   int k = 0;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
     const int s = k % a.stages;
@@ -223,14 +223,14 @@ __global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
           if (f.W > 32) seq_fast_step<false, true>(f, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
           else seq_fast_step<false, false>(f, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * kStagedConsumerWarps) : "memory");   // step boundary
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kSeqWarps) : "memory");   // step boundary
         if (st_i == 0 && cw == 0 && lane == 0) mbar_arrive(&empty[s]);   // stage buffer consumed
         continue;
       }
       // work items: (plane, output row, 32-column chunk); lane = output column
       const int nchunk = (st.Wo + 31) / 32;
       const int items = np * st.Ho * nchunk;
-      for (int it = cw; it < items; it += kStagedConsumerWarps) {
+      for (int it = cw; it < items; it += kSeqWarps) {
         const int cc = it % nchunk;
         const int i = (it / nchunk) % st.Ho;
         const int p = it / (nchunk * st.Ho);
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kStagedThreads) seq_staged(SeqArgs a) {
         if (last) __stcs(a.out + plane * (int64_t)HWo + i * st.Wo + j, r);
         else out_buf[p * HWo + i * st.Wo + j] = r;
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * kStagedConsumerWarps) : "memory");   // step boundary
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kSeqWarps) : "memory");   // step boundary
       if (st_i == 0 && cw == 0 && lane == 0) mbar_arrive(&empty[s]);   // stage buffer consumed
     }
   }
@@ -257,7 +257,7 @@ cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st) {
   const size_t smem = seq_smem(a);
   cudaError_t e = cudaFuncSetAttribute((void*)seq_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl((void*)seq_staged, dim3(grid), dim3(kStagedThreads), args, smem, st);
+  return launch_pdl((void*)seq_staged, dim3(grid), dim3(kSeqThreads), args, smem, st);
 }
 
 int seq_max_blocks_per_sm(const SeqArgs& a) {
@@ -265,7 +265,7 @@ int seq_max_blocks_per_sm(const SeqArgs& a) {
   int n = 0;
   if (cudaFuncSetAttribute((void*)seq_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, (void*)seq_staged, kStagedThreads, smem) != cudaSuccess) n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, (void*)seq_staged, kSeqThreads, smem) != cudaSuccess) n = 0;
   return n;
 }
 
