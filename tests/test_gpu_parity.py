@@ -363,6 +363,25 @@ def test_graph_matches_sequential_execution(cuda_dev, oracle_lib):
     bs.bs_graph_destroy(g)
 
 
+@pytest.mark.parametrize("shape,pool", [((64, 64, 111, 111), (3, 2, 1)), ((96, 48, 57, 57), (2, 2, 0)),
+                                        ((32, 256, 27, 27), (3, 1, 1)), ((128, 160, 7, 7), (7, 7, 0))])
+def test_staged_large_odd_shapes_sampled(shape, pool, cuda_dev, oracle_lib):
+    """The staged kernel at sizes where the planner picks one CTA per SM / round-robin tiles /
+    padded windows, images checked against the oracle one by one."""
+    bs = _bs()
+    k, s_, p = pool
+    layers = [synth.batchnorm(shape[1], 11, signed_gamma=True), synth.relu(), synth.maxpool(k, s_, p)]
+    plan = bs.bs_plan_create(layers, shape)
+    assert bs.bs_plan_query_launch(plan, 0)["kernel_name"] == "pool_staged_tma"
+    x = synth.uniform_torch(5, shape, device="cuda")
+    out = torch.empty(bs.bs_plan_query(plan)["out"], device="cuda")
+    bs.bs_execute(plan, x, out)
+    torch.cuda.synchronize()
+    for n in sorted({0, shape[0] // 3, shape[0] - 1}):
+        ref = oracle.run_bf(layers, x[n:n + 1].cpu().numpy())
+        U.check(out[n:n + 1].cpu().numpy(), ref, layers, f"{shape} {pool} image {n}")
+
+
 def test_empty_batch(cuda_dev):
     """An empty batch executes as a no-op through every entry point (NULL pointers allowed)."""
     bs = _bs()
