@@ -419,23 +419,33 @@ def main():
     probe = int(min(h2d, 256 << 20))   # (at most 256 MB of pinned memory for the probe)
     hb = torch.empty(probe // 4, dtype=torch.float32).pin_memory()
     db = torch.empty(probe // 4, dtype=torch.float32, device=dev)
-    pcie_gbs = 0.0
+    pcie_gbs = d2h_gbs = 0.0
     with torch.cuda.stream(stream):
-        for r in range(7):   # 2 warm-up copies, then the best of 5
+        for r in range(7):   # 2 warm-up copies each way, then the best of 5
             a.record(stream)
             db.copy_(hb, non_blocking=True)
             b.record(stream)
             torch.cuda.synchronize()
             if r >= 2:
                 pcie_gbs = max(pcie_gbs, probe / (a.elapsed_time(b) / 1e3) / 1e9)
+            a.record(stream)
+            hb.copy_(db, non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if r >= 2:
+                d2h_gbs = max(d2h_gbs, probe / (a.elapsed_time(b) / 1e3) / 1e9)
     del hb, db
     e2e_h2d_gbs = h2d / (e2e_ms / e2e_steps / 1e3) / 1e9
+    # the binding direction: the step cannot beat max(H2D time, D2H time) at the probed rates
+    t_bound = max(h2d / (pcie_gbs * 1e9), d2h / (d2h_gbs * 1e9))
+    bound_frac = t_bound / (e2e_ms / e2e_steps / 1e3)
     e2e = {"value": images / (e2e_ms / e2e_steps / 1e3), "unit": "images/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
            "path": "bs_execute_host: pinned host -> device copy, kernels, device -> host copy, pipelined per chunk",
-           "roofline": {"bound": "pcie_h2d", "achieved_gbs": e2e_h2d_gbs, "peak_gbs": pcie_gbs,
-                        "frac": e2e_h2d_gbs / pcie_gbs,
-                        "peak_source": "measured: best of 5 pinned host -> device torch copies of the same bytes (<= 256 MB)"}}
+           "roofline": {"bound": "pcie_h2d" if h2d / pcie_gbs >= d2h / d2h_gbs else "pcie_d2h",
+                        "achieved_gbs": e2e_h2d_gbs, "peak_gbs": pcie_gbs, "d2h_peak_gbs": d2h_gbs,
+                        "frac": bound_frac,
+                        "peak_source": "measured: best of 5 pinned host <-> device torch copies (<= 256 MB each way); frac = max(H2D, D2H) time at those rates / step time"}}
 
     # ---- layer-by-layer torch eager on the same GPU (the paper's comparison system, re-hosted)
     lbl = None
