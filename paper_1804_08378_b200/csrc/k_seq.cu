@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
   uint64_t* empty = full + 8;
   const size_t tile_stride = pool_staged_stride(a.tile_planes, a.in_plane);
   unsigned char* stage0 = smem + 128;
-  float* work[2] = {(float*)(stage0 + (size_t)a.stages * tile_stride),
-                    (float*)(stage0 + (size_t)a.stages * tile_stride) + a.work_floats};
+  // the two ping-pong work buffers (selected by arithmetic, not a local array: no local memory)
+  float* const work0 = (float*)(stage0 + (size_t)a.stages * tile_stride);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (int)a.n_tiles;
   const int HW0 = a.in_plane;
@@ -208,8 +208,8 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
     for (int st_i = 0; st_i < a.n_steps; ++st_i) {
       const SeqStepDev& st = a.steps[st_i];
       const bool last = st_i == a.n_steps - 1;
-      const float* in_buf = st_i == 0 ? src_base : work[(st_i - 1) & 1];
-      float* out_buf = work[st_i & 1];
+      const float* in_buf = st_i == 0 ? src_base : work0 + ((st_i - 1) & 1) * a.work_floats;
+      float* out_buf = work0 + (st_i & 1) * a.work_floats;
       const int HWi = st.H * st.W, HWo = st.Ho * st.Wo;
       if (fast_tab[st_i].W > 0) {
         const SeqFastStep& f = fast_tab[st_i];
