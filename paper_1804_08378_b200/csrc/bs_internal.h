@@ -144,7 +144,6 @@ size_t pool_staged_smem(int tile_planes, int HW, int HWo, int stages);
 __host__ __device__ inline size_t pool_staged_stride(int tile_planes, int HW) {
   return ((size_t)tile_planes * HW * 4 + 16 + 127) / 128 * 128;
 }
-int pool_staged_unroll(int k, int s);
 int pool_max_blocks_per_sm(int kernel_kind, const PoolArgs& a, int block);
 
 }  // namespace bs

@@ -32,7 +32,6 @@ size_t pool_staged_smem(int tile_planes, int HW, int HWo, int stages) {
   return kStagedHeader + (size_t)stages * pool_staged_stride(tile_planes, HW);
 }
 
-int pool_staged_unroll(int k, int s) { (void)k; (void)s; return 1; }
 
 template <int KH, int KW, int SH, int SW, bool IS_MAX, bool PAD, int PC, int OC>
 __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
@@ -177,11 +176,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
 #ifdef BS_DBG_NOSTORE
         if (res == 1234.5f)
 #endif
-#ifdef BS_DBG_L2STORE
-        __stcs(a.out + (((uintptr_t)op / 4) & 0x3FFF), res);
-#else
         __stcs(op, res);
-#endif
         op += a.Wo;
       };
       if (!PAD) {
