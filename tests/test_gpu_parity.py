@@ -364,7 +364,8 @@ def test_graph_matches_sequential_execution(cuda_dev, oracle_lib):
 
 
 @pytest.mark.parametrize("shape,pool", [((64, 64, 111, 111), (3, 2, 1)), ((96, 48, 57, 57), (2, 2, 0)),
-                                        ((32, 256, 27, 27), (3, 1, 1)), ((128, 160, 7, 7), (7, 7, 0))])
+                                        ((32, 256, 27, 27), (3, 1, 1)), ((128, 160, 7, 7), (7, 7, 0)),
+                                        ((32, 64, 101, 101), (3, 1, 1)), ((16, 32, 151, 151), (3, 2, 1))])
 def test_staged_large_odd_shapes_sampled(shape, pool, cuda_dev, oracle_lib):
     """The staged kernel at sizes where the planner picks one CTA per SM / round-robin tiles /
     padded windows, images checked against the oracle one by one."""
