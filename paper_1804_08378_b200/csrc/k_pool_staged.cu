@@ -25,6 +25,9 @@ namespace bs {
 //    slide along in registers, outputs are stored to HBM with st.global.cs.
 //  * Tiles may start on any float: the 16-byte-aligned middle is bulk-copied, the <= 6 edge
 //    floats use 4-byte cp.async tracked by the same full barrier.
+//  * The ring holds ~104 KB of tiles per SM (bs_api.cpp size_stages): measured on B200, more
+//    bytes in flight is slower, and one CTA per SM beats two for big tiles on long kernels.
+//    Waits sleep (mbarrier.try_wait with a suspend-time hint) instead of spinning.
 
 // barriers | `stages` input stages
 size_t pool_staged_smem(int tile_planes, int HW, int HWo, int stages) {
