@@ -239,3 +239,24 @@ def test_staged_ring_policy(bs):
     assert info["alexnet_s3"]["grid"] == 2 * sms                                       # 13.5 KB tiles
     for li in info.values():
         assert 1 <= li["rows_per_task"] <= li["out"][2]
+
+
+def _build_c_example(bs, tmp_path):
+    exe = str(tmp_path / "stack_demo")
+    lib_dir = os.path.dirname(bs.LIB_PATH)
+    cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+           "-I", "/usr/local/cuda/include", os.path.join(ROOT, "examples", "stack_demo.c"), "-L", lib_dir,
+           "-lbrainslug", "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib_dir}", "-o", exe]
+    subprocess.check_call(cmd)
+    return exe
+
+
+def test_c_abi_usable_from_plain_c(bs, tmp_path):
+    """include/bs.h is plain C99 and libbrainslug.so links into a C program (examples/)."""
+    assert os.path.exists(_build_c_example(bs, tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_example_runs(bs, tmp_path, cuda_dev):
+    out = subprocess.check_output([_build_c_example(bs, tmp_path), "4"]).decode()
+    assert "OK" in out and "-> (4,64,56,56)" in out, out
