@@ -228,11 +228,12 @@ class BrainSlugStack(nn.Module):
         x = x.contiguous()
         ops = [o.contiguous() for o in operands]
         key = (tuple(x.shape), x.device.index)
-        plan = self._plans.get(key)
-        if plan is None:
+        entry = self._plans.get(key)
+        if entry is None:
             plan = bs_plan_create(self._resolved_layers(x.shape), x.shape, {"device": x.device.index})
-            self._plans[key] = plan
-        out = torch.empty(bs_plan_query(plan)["out"], device=x.device, dtype=torch.float32)
+            entry = self._plans[key] = (plan, tuple(bs_plan_query(plan)["out"]))
+        plan, out_shape = entry
+        out = torch.empty(out_shape, device=x.device, dtype=torch.float32)
         bs_execute_ex(plan, [x] + ops, out, torch.cuda.current_stream(x.device))
         return out
 
