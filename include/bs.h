@@ -23,8 +23,11 @@
  *  - bs_execute* only ENQUEUE work on the caller's stream: no allocation, no host sync,
  *    no host<->device copy (except bs_execute_host, whose job is exactly those copies).
  *    Asynchronous device faults surface at the caller's next synchronisation.
- *  - Plans are immutable after creation; concurrent bs_execute on different streams is
- *    safe.  bs_plan_create is reentrant.
+ *  - Plans are immutable after creation.  Concurrent bs_execute / bs_execute_ex of a plan
+ *    with n_launches == 1 on different streams is safe.  A plan with n_launches > 1 (its
+ *    serialised sequences share plan-owned intermediates) and bs_execute_host (plan-owned
+ *    copy streams and events) must not run concurrently with itself: use one plan per
+ *    stream there.  bs_plan_create is reentrant.
  */
 #ifndef BS_H
 #define BS_H
