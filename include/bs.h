@@ -97,7 +97,8 @@ typedef struct {
     int32_t max_steps_per_sequence; /* 0 = unlimited (up to 16 steps and what fits on chip);
                                        1 and 5 mirror the paper's policies.  A
                                        sequence of >= 2 steps runs on-chip in one launch */
-    int32_t threads_per_block;      /* 0 = planner default (multiple of 32, <= 1024) */
+    int32_t threads_per_block;      /* must be 0: every kernel has a fixed block size tuned for
+                                       sm_100a (256 or 32 x 9); other values -> INVALID_ARGUMENT */
     int32_t force_rows_per_task;    /* 0 = planner; >0 forces the output-row band of a pool
                                        tile (tests use it: results must not depend on tiling) */
     int32_t force_outputs_per_group;/* 0 = planner; >0 forces output columns per lane group */

@@ -864,6 +864,9 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
   std::memset(&o, 0, sizeof o);
   o.device = -1;
   if (opts) o = *opts;
+  if (o.threads_per_block != 0)
+    return fail(BS_ERR_INVALID_ARGUMENT, "threads_per_block=%d: block sizes are fixed per kernel (pass 0)",
+                o.threads_per_block);
 
   // an empty batch (N = 0) is valid: plan the geometry of one image, execute nothing
   const bool empty_batch = input.n == 0;

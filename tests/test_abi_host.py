@@ -260,3 +260,9 @@ def test_c_abi_usable_from_plain_c(bs, tmp_path):
 def test_c_example_runs(bs, tmp_path, cuda_dev):
     out = subprocess.check_output([_build_c_example(bs, tmp_path), "4"]).decode()
     assert "OK" in out and "-> (4,64,56,56)" in out, out
+
+
+def test_threads_per_block_is_not_configurable(bs):
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_plan_create([synth.relu()], (1, 1, 4, 4), {"host_only": 1, "threads_per_block": 128})
+    assert e.value.status == 2 and "threads_per_block" in str(e.value)
