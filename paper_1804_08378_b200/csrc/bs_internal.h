@@ -52,6 +52,7 @@ struct EwArgs {
   int32_t hw_ge4;           // H*W >= 4 (a float4 spans at most 2 planes)
   const float* add0_ptr;    // operand of the prefetched ADD (add_slot 0), or nullptr
   int32_t prog_class;       // ProgClass of prog
+  int32_t unroll;           // float4s per thread per iteration: 4, or 1 for small tensors
   OpProgram prog;
 };
 

@@ -3,7 +3,7 @@
 
 namespace bs {
 
-template <int PC>
+template <int PC, int U>
 __global__ void __launch_bounds__(kEwBlock) ew_kernel(EwArgs a) {
   pdl_wait();                 // previous kernel on the stream complete + visible
   pdl_launch_dependents();
@@ -15,23 +15,23 @@ __global__ void __launch_bounds__(kEwBlock) ew_kernel(EwArgs a) {
   const uint32_t HW = a.hw.d, C = a.c.d;
   const float2* aff0p = (PC == PC_AFFINE || PC == PC_AFFINE_RELU) ? P.affine[0] : nullptr;
 
-  const uint32_t stride = gridDim.x * kEwBlock * kEwUnroll;
-  for (uint32_t base = blockIdx.x * kEwBlock * kEwUnroll + threadIdx.x; base < nv; base += stride) {
-    float4 x[kEwUnroll], ad[kEwUnroll];
+  const uint32_t stride = gridDim.x * kEwBlock * U;
+  for (uint32_t base = blockIdx.x * kEwBlock * U + threadIdx.x; base < nv; base += stride) {
+    float4 x[U], ad[U];
 #pragma unroll
-    for (int k = 0; k < kEwUnroll; ++k) {
+    for (int k = 0; k < U; ++k) {
       const uint32_t vi = base + k * kEwBlock;
       if (vi < nv) x[k] = ld_stream4(a.in + v_begin + 4u * vi);
     }
     if (PC == PC_GENERIC && a.add0_ptr != nullptr) {
 #pragma unroll
-      for (int k = 0; k < kEwUnroll; ++k) {
+      for (int k = 0; k < U; ++k) {
         const uint32_t vi = base + k * kEwBlock;
         if (vi < nv) ad[k] = ld_stream4(a.add0_ptr + v_begin + 4u * vi);
       }
     }
 #pragma unroll
-    for (int k = 0; k < kEwUnroll; ++k) {
+    for (int k = 0; k < U; ++k) {
       const uint32_t vi = base + k * kEwBlock;
       if (vi >= nv) continue;
       const uint32_t e = v_begin + 4u * vi;
@@ -124,19 +124,24 @@ __global__ void __launch_bounds__(kEwBlock) ew_kernel(EwArgs a) {
 }
 
 
-static void* ew_fn(int pc) {
+template <int U>
+static void* ew_fn_u(int pc) {
   switch (pc) {
-    case PC_RELU: return (void*)ew_kernel<PC_RELU>;
-    case PC_AFFINE: return (void*)ew_kernel<PC_AFFINE>;
-    case PC_AFFINE_RELU: return (void*)ew_kernel<PC_AFFINE_RELU>;
-    default: return (void*)ew_kernel<PC_GENERIC>;
+    case PC_RELU: return (void*)ew_kernel<PC_RELU, U>;
+    case PC_AFFINE: return (void*)ew_kernel<PC_AFFINE, U>;
+    case PC_AFFINE_RELU: return (void*)ew_kernel<PC_AFFINE_RELU, U>;
+    default: return (void*)ew_kernel<PC_GENERIC, U>;
   }
 }
+
+// U = float4s per thread per iteration: 4 (64 B in flight per thread) for large tensors, 1 for
+// small ones, which then spread over 4x more threads (one wave of latency-bound loads).
+static void* ew_fn(int pc, int unroll = kEwUnroll) { return unroll == 1 ? ew_fn_u<1>(pc) : ew_fn_u<kEwUnroll>(pc); }
 
 cudaError_t launch_ew(const EwArgs& a, int grid, int block, cudaStream_t st) {
   (void)block;
   void* args[] = {(void*)&a};
-  return launch_pdl(ew_fn(a.prog_class), dim3(grid), dim3(kEwBlock), args, 0, st);
+  return launch_pdl(ew_fn(a.prog_class, a.unroll), dim3(grid), dim3(kEwBlock), args, 0, st);
 }
 
 int ew_max_blocks_per_sm(int pc) {
