@@ -347,7 +347,9 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
   // 24 KB: 20.5 us on s1), so one CTA per SM for tiles >= 20 KB when each SM has >= 12 tiles,
   // two (more consumer warps per byte) otherwise (s3, 13.5 KB tiles: 2 x 4 stages 6.1 us vs
   // 1 x 7 stages 6.5 us; DenseNet final, 31 KB tiles, 11 per SM: 2 CTAs).
-  constexpr int64_t kInflightPerSm = 104 * 1024;
+  // (read-dominated pools -- global averages, output < 1/8 of the input -- gain from twice that:
+  // DenseNet-121 final 7x7 average, 2 x 3 x 31 KB: 10.7 us vs 11.6 us at 2 x 2)
+  const int64_t kInflightPerSm = 8 * st.out.h * st.out.w < HW ? 208 * 1024 : 104 * 1024;
   const int64_t tiles_per_sm = (n_planes + bP - 1) / bP / std::max(1, num_sms);
   // one CTA per SM only for big tiles, long kernels and pools that shrink the plane (stride >= 2:
   // few outputs per staged byte); stride-1 pools (the §5.1 block: one output per input) need the
