@@ -118,3 +118,49 @@ def test_optimized_network_matches_eager(net, cuda_dev):
     assert torch.allclose(got, ref, rtol=1e-4, atol=1e-4 * max(1.0, scale)), (got - ref).abs().max().item()
     with torch.no_grad():   # an empty batch goes through every stack as a no-op
         assert gm(x[:0]).shape == (0,) + tuple(ref.shape[1:])
+
+
+class _Mixed(torch.nn.Module):
+    """Every optimizable kind the front-end knows: BN, ReLU (module, functional, method), MaxPool,
+    AvgPool, Dropout, scalar multiply, residual add, global average pool."""
+
+    def __init__(self):
+        super().__init__()
+        self.conv1 = torch.nn.Conv2d(3, 8, 3, padding=1)
+        self.bn = torch.nn.BatchNorm2d(8)
+        self.pool = torch.nn.MaxPool2d(3, 2, 1)
+        self.conv2 = torch.nn.Conv2d(8, 8, 1)
+        self.avg = torch.nn.AvgPool2d(2, 2, count_include_pad=False)
+        self.drop = torch.nn.Dropout(0.5)
+        self.gap = torch.nn.AdaptiveAvgPool2d(1)
+        self.fc = torch.nn.Linear(8, 4)
+
+    def forward(self, x):
+        x = self.pool(torch.nn.functional.relu(self.bn(self.conv1(x))))   # [BN, relu, maxpool]
+        y = self.conv2(x)
+        y = (y * 0.5 + x).relu()                                           # [scale, add, relu]
+        y = self.gap(self.drop(self.avg(y)))                               # (continues the stack)
+        return self.fc(torch.flatten(y, 1))
+
+
+def test_mixed_model_stacks():
+    from paper_1804_08378_b200 import frontend as fe
+    d = fe.summary(_Mixed().eval())
+    assert d["signatures"] == ["[batchnorm,relu,maxpool]", "[scale,add,relu,avgpool,copy,avgpool]"]
+    assert d["opt_layers"] == 8   # the residual add is not a layer
+
+
+@pytest.mark.gpu
+def test_mixed_model_matches_eager(cuda_dev):
+    from paper_1804_08378_b200 import frontend as fe
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.manual_seed(3)
+    m = _Mixed().eval()
+    _randomise_bn(m, 4)
+    m = m.cuda()
+    x = torch.randn(3, 3, 33, 31, device="cuda")
+    with torch.no_grad():
+        ref = m(x)
+        got = fe.optimize(m)(x)
+    assert torch.allclose(got, ref, rtol=1e-4, atol=1e-5), (got - ref).abs().max().item()
