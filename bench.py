@@ -301,6 +301,19 @@ def main():
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
 
+    # per-step min / median (SURVEY §8(d) protocol), outside the timed region: 20 steps each
+    # bracketed by its own events (serialised, so each includes its own ramp and drain)
+    per_step = []
+    with torch.cuda.stream(stream):
+        for k in range(20):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run_step(k)
+            e1.record(stream)
+            e1.synchronize()
+            per_step.append(e0.elapsed_time(e1))
+    step_min, step_med = float(np.min(per_step)), float(np.median(per_step))
+
     # dominant kernel alone: D back-to-back launches over rotating buffer sets (one graph),
     # CUDA events on the launching stream around the replays -> average launch duration
     D = max(4, min(50, int(4 * l2 // max(1, dom_bytes)) + 4))
@@ -511,7 +524,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_isolated": {"min": step_min, "median": step_med, "n": len(per_step)},
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 seeded NCHW fp32, BN params per SURVEY §8(d))",
             "config": {"workload": args.workload, "baseline_config_index": CONFIG_INDEX[args.workload],
                        "global_batch": images, "per_gpu_batch": batch, "stacks_per_step": len(inst),
