@@ -111,7 +111,12 @@ typedef struct {
                                        the 16-byte bulk-copy granularity */
     int32_t force_stages;           /* 0 = planner; 2..8: shared-memory ring depth of the staged
                                        kernel */
-    int32_t reserved[3];
+    int32_t smem_budget_bytes;      /* 0 = planner default (<= 220 KB per CTA); > 0: the most
+                                       dynamic shared memory per CTA the plan may use -- the
+                                       paper's per-step cache budget.  Staged pools
+                                       use fewer ring stages (or the global-memory walker) and
+                                       on-chip sequences split earlier to fit it */
+    int32_t reserved[2];
 } bs_plan_options;
 
 /* Whole-plan summary. */

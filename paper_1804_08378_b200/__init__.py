@@ -60,7 +60,8 @@ class bs_plan_options(ctypes.Structure):
                 ("max_steps_per_sequence", ctypes.c_int32), ("threads_per_block", ctypes.c_int32),
                 ("force_rows_per_task", ctypes.c_int32), ("force_outputs_per_group", ctypes.c_int32),
                 ("force_generic", ctypes.c_int32), ("force_tile_planes", ctypes.c_int32),
-                ("force_stages", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("force_stages", ctypes.c_int32), ("smem_budget_bytes", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class bs_plan_info(ctypes.Structure):
@@ -202,7 +203,8 @@ def bs_plan_create(layers: Sequence, input_shape, opts: Optional[dict] = None) -
         o = bs_plan_options()
         o.device = opts.get("device", -1)
         for k in ("host_only", "max_steps_per_sequence", "threads_per_block", "force_rows_per_task",
-                  "force_outputs_per_group", "force_generic", "force_tile_planes", "force_stages"):
+                  "force_outputs_per_group", "force_generic", "force_tile_planes", "force_stages",
+                  "smem_budget_bytes"):
             setattr(o, k, int(opts.get(k, 0)))
     h = _P()
     st = _lib.bs_plan_create(arr, len(layers), bs_shape(*[int(v) for v in input_shape]),

@@ -309,6 +309,11 @@ void set_device_programs(Launch& l) {
 // barrier work).  Ring depth: as many stages as fit two CTAs per SM (<= 8).  False if one
 // plane group is too large to stage.
 constexpr int64_t kStagedTileMax = 32 * 1024;
+// Dynamic shared memory a plan may use per CTA (bs_plan_options.smem_budget_bytes).
+int64_t smem_cap(const bs_plan_options& o) {
+  return o.smem_budget_bytes > 0 ? std::min<int64_t>(o.smem_budget_bytes, 220 * 1024) : 220 * 1024;
+}
+
 bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_sms) {
   const Step& st = l.step;
   const int64_t HW = st.in.h * st.in.w, Ho = st.out.h;
@@ -359,7 +364,8 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
   l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kStagedMaxStages,
                                                             (kInflightPerSm / l.ctas_per_sm + stride / 2) / stride));
   if (o.force_stages >= 2) l.stages = std::min(kStagedMaxStages, o.force_stages);
-  if ((int64_t)l.stages * stride > 220 * 1024) l.stages = (int32_t)((220 * 1024) / stride);
+  const int64_t cap = smem_cap(o) - kStagedHeader;
+  if ((int64_t)l.stages * stride > cap) l.stages = (int32_t)(cap / stride);
   if (l.stages < 2) return false;
   l.U = 1;
   return true;
@@ -468,10 +474,10 @@ int64_t seq_bytes(const std::vector<Step>& st, size_t a, size_t b, int64_t P, in
 // sequence still fits on chip -- here: whole planes of the first input and of every
 // intermediate in shared memory (no halos) -- and the policy's step limit allows it.
 // A step with an ADD operand (per-execute pointers) is kept in a sequence of its own.
-bool seq_fits(const std::vector<Step>& st, size_t a, size_t b) {
+bool seq_fits(const std::vector<Step>& st, size_t a, size_t b, int64_t cap) {
   for (size_t k = a; k < b; ++k)
     if (has_add(st[k])) return false;
-  return seq_bytes(st, a, b, 1, 2, nullptr) <= 220 * 1024;
+  return seq_bytes(st, a, b, 1, 2, nullptr) <= cap;
 }
 
 void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& o) {
@@ -481,7 +487,7 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
   std::vector<std::pair<size_t, size_t>> seqs;
   for (size_t a = 0; a < steps.size();) {
     size_t b = a + 1;
-    while (b < steps.size() && b - a < max_steps && seq_fits(steps, a, b + 1)) ++b;
+    while (b < steps.size() && b - a < max_steps && seq_fits(steps, a, b + 1, smem_cap(o))) ++b;
     seqs.emplace_back(a, b);
     a = b;
   }
@@ -509,11 +515,12 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
       // planes per tile: the most that keep two CTAs per SM (else one), >= 8 tiles per CTA
       const int64_t n_planes = steps[a].in.n * steps[a].in.c;
       int64_t P = 1;
-      while (P * 2 <= n_planes / (8 * 2 * p->num_sms) && seq_bytes(steps, a, b, P * 2, 2, nullptr) <= 110 * 1024) P *= 2;
+      const int64_t half = std::min<int64_t>(110 * 1024, smem_cap(o));
+      while (P * 2 <= n_planes / (8 * 2 * p->num_sms) && seq_bytes(steps, a, b, P * 2, 2, nullptr) <= half) P *= 2;
       if (o.force_tile_planes > 0) P = o.force_tile_planes;
       int stages = 2;
-      while (stages < 4 && seq_bytes(steps, a, b, P, stages + 1, nullptr) <= 110 * 1024) ++stages;
-      if (seq_bytes(steps, a, b, P, stages, nullptr) > 220 * 1024) { P = 1; stages = 2; }
+      while (stages < 4 && seq_bytes(steps, a, b, P, stages + 1, nullptr) <= half) ++stages;
+      if (seq_bytes(steps, a, b, P, stages, nullptr) > smem_cap(o)) { P = 1; stages = 2; }
       int64_t wf = 0;
       seq_bytes(steps, a, b, P, stages, &wf);
       l.tile_planes = (int32_t)P;

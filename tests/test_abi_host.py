@@ -266,3 +266,16 @@ def test_threads_per_block_is_not_configurable(bs):
     with pytest.raises(bs.BsError) as e:
         bs.bs_plan_create([synth.relu()], (1, 1, 4, 4), {"host_only": 1, "threads_per_block": 128})
     assert e.value.status == 2 and "threads_per_block" in str(e.value)
+
+
+def test_smem_budget_option(bs):
+    """smem_budget_bytes caps the shared memory per CTA: on-chip sequences split, staged pools
+    drop to fewer stages or to the global-memory walker (the paper's cache budget)."""
+    sec = synth.synthetic51(4, batch=2, C=3, H=56)
+    assert bs.bs_plan_query(host_plan(bs, sec.layers, sec.shape))["n_launches"] == 1
+    small = bs.bs_plan_create(sec.layers, sec.shape, {"host_only": 1, "smem_budget_bytes": 40 * 1024})
+    assert bs.bs_plan_query(small)["n_launches"] == 4
+    s1 = synth.workload("alexnet")[0]
+    assert bs.bs_plan_query_launch(host_plan(bs, s1.layers, s1.shape), 0)["kernel"] == 6
+    p = bs.bs_plan_create(s1.layers, s1.shape, {"host_only": 1, "smem_budget_bytes": 40 * 1024})
+    assert bs.bs_plan_query_launch(p, 0)["kernel"] == 2      # 2 x 24 KB stages do not fit 40 KB

@@ -383,6 +383,17 @@ def test_staged_large_odd_shapes_sampled(shape, pool, cuda_dev, oracle_lib):
         U.check(out[n:n + 1].cpu().numpy(), ref, layers, f"{shape} {pool} image {n}")
 
 
+@pytest.mark.parametrize("budget", [24 * 1024, 40 * 1024, 64 * 1024])
+def test_smem_budget_results_unchanged(budget, cuda_dev, oracle_lib):
+    """A shared-memory budget changes sequences / kernels, never the results."""
+    sec = synth.synthetic51(6, batch=2, C=3, H=41)
+    x = synth.uniform_np(31, int(np.prod(sec.shape))).reshape(sec.shape)
+    compare(sec.layers, x, opts={"smem_budget_bytes": budget}, ctx=f"sec51 budget {budget}")
+    s1 = synth.workload("alexnet", batch=2)[0]
+    x = synth.uniform_np(32, int(np.prod(s1.shape))).reshape(s1.shape)
+    compare(s1.layers, x, opts={"smem_budget_bytes": budget}, ctx=f"alexnet_s1 budget {budget}")
+
+
 def test_empty_batch(cuda_dev):
     """An empty batch executes as a no-op through every entry point (NULL pointers allowed)."""
     bs = _bs()
