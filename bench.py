@@ -549,6 +549,11 @@ def main():
             "clocks": clk.summary(),
             "layer_by_layer_torch": lbl,
             "checksums": checksums, "outputs_finite": finite,
+            # the paper's own numbers, quoted with their hardware (context, not targets)
+            "paper_context": {"best_whole_network_speedup_gpu": "35.7 % (GTX 1080 Ti, PyTorch 0.3.0 + cuDNN, fp32)",
+                              "best_whole_network_speedup_cpu": "41.1 % (Xeon E5-2690v4, ISPC + TBB)",
+                              "synthetic_blocks_gpu": "1.4-2.2x vs PyTorch (GTX 1080 Ti)",
+                              "source": "PAPER.md P:L27-29, P:L689, P:L953"},
             "per_stack": per_stack,
         }
         s = json.dumps(line)
