@@ -110,6 +110,16 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def time_oracle(cases, budget_s: float, max_images: int):
     """The oracle as it stands (single thread) on whole images of the workload."""
     import oracle
@@ -509,7 +519,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, n, T = time_oracle(cases, args.cpu_budget, 1 << 20)
-        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle",
+        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle", "host_cores": os.cpu_count(),
+               "host_cpu": _cpu_model(),
                "sample": f"{n} synthetic images shaped like the batch-{batch} {args.workload} workload (all stacks), "
                          f"breadth-first C oracle, single thread, {T:.1f} s"}
 
