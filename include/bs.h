@@ -150,8 +150,13 @@ typedef struct {
     int32_t outputs_per_group;      /* output columns produced by one lane group */
     int32_t rows_per_task;          /* output rows walked by one warp task */
     int32_t halo_rows;              /* input rows re-read between row bands (k - s, >= 0) */
-    int64_t n_tasks;                /* warp tasks */
+    int64_t n_tasks;                /* warp tasks (kernels 2-5), staged tiles (6, 7) */
     int64_t alg_bytes_read, alg_bytes_written;
+    int32_t smem_bytes;             /* dynamic shared memory per CTA (0 for kernels 1-5) */
+    int32_t tile_planes;            /* kernels 6/7: (n, c) planes per staged tile, else 0 */
+    int32_t tile_rows;              /* kernel 7 with row-band tiles: output rows per tile, else 0
+                                       (whole planes) */
+    int32_t stages;                 /* kernels 6/7: shared-memory ring depth, else 0 */
 } bs_launch_info;
 
 /*

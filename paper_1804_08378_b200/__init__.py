@@ -81,7 +81,9 @@ class bs_launch_info(ctypes.Structure):
                 ("grid", ctypes.c_int32), ("block", ctypes.c_int32), ("groups_per_warp", ctypes.c_int32),
                 ("outputs_per_group", ctypes.c_int32), ("rows_per_task", ctypes.c_int32),
                 ("halo_rows", ctypes.c_int32), ("n_tasks", ctypes.c_int64),
-                ("alg_bytes_read", ctypes.c_int64), ("alg_bytes_written", ctypes.c_int64)]
+                ("alg_bytes_read", ctypes.c_int64), ("alg_bytes_written", ctypes.c_int64),
+                ("smem_bytes", ctypes.c_int32), ("tile_planes", ctypes.c_int32), ("tile_rows", ctypes.c_int32),
+                ("stages", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p

@@ -304,7 +304,8 @@ void set_device_programs(Launch& l) {
 // chosen so that the 8 consumer warps share every tile evenly.  A tile holds I =
 // ceil(P/G) * n_cc * ceil(Ho/R) items and each warp walks ceil(I/8) of them in turn, each item
 // reducing R*s + (k-s) input rows; the choice minimises that per-tile walk per staged plane,
-// (I <= 16: a warp holds at most two items), with a mild preference for 12-32 KB tiles (small enough for >= 3 ring stages at two CTAs per
+// (I <= 16 where possible: a warp's two items are then decoded once per CTA; wider planes take
+// more items per warp), with a mild preference for 12-32 KB tiles (small enough for >= 3 ring stages at two CTAs per
 // SM and for the last tile of a CTA's range to be cheap; large enough to amortise the per-tile
 // barrier work).  Ring depth: as many stages as fit two CTAs per SM (<= 8).  False if one
 // plane group is too large to stage.
@@ -323,6 +324,9 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
   const int64_t max_groups = (n_planes + G - 1) / G;
   double best = 1e300;
   int64_t bP = G, bR = Ho;
+  // first pass: tiles of <= 16 items (a warp's two items decoded once per CTA); if none exists
+  // (planes wider than 16 column chunks, or a forced narrow column group) any item count
+  for (int pass = 0; pass < 2 && best == 1e300; ++pass)
   for (int64_t m = 1; m <= max_groups && (m == 1 || m * G * plane_bytes <= kStagedTileMax); ++m) {
     if (o.force_tile_planes > 0 && m != std::max<int64_t>(1, o.force_tile_planes / G)) continue;
     for (int64_t R = 1; R <= Ho; ++R) {
@@ -330,7 +334,7 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
       if (R > 1 && (Ho + R - 2) / (R - 1) == nrb) continue;     // same band count as R-1
       if (o.force_rows_per_task > 0 && R != std::min<int64_t>(Ho, o.force_rows_per_task)) continue;
       const int64_t I = m * ncc * nrb;
-      if (I > 2 * NC) continue;                                  // the kernel holds <= 2 items per warp
+      if (pass == 0 && I > 2 * NC) continue;                     // <= 2 items per warp
       const double walk = (double)((I + NC - 1) / NC) * (double)(R * st.sh + carry);
       const int64_t T = m * G * plane_bytes;
       const double size_f = T < 8192 ? 1.25 : T < 12288 ? 1.05 : T > kStagedTileMax ? 1.1 : 1.0;
@@ -691,6 +695,15 @@ void fill_launch_info(bs_plan* p) {
       li.n_tasks = (n_planes + l.tile_planes - 1) / l.tile_planes;
       li.grid = (int)std::min<int64_t>(li.n_tasks, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
       li.block = kSeqThreads;
+      SeqArgs probe;
+      std::memset(&probe, 0, sizeof probe);
+      probe.tile_planes = l.tile_planes;
+      probe.stages = l.stages;
+      probe.work_floats = l.seq_work_floats;
+      probe.in_plane = (int32_t)(s.in.h * s.in.w);
+      li.smem_bytes = (int32_t)seq_smem(probe);
+      li.tile_planes = l.tile_planes;
+      li.stages = l.stages;
     } else {
       li.groups_per_warp = l.G;
       li.outputs_per_group = l.Jg;
@@ -699,6 +712,12 @@ void fill_launch_info(bs_plan* p) {
       li.n_tasks = pool_tasks(l, n_planes);
       li.grid = pool_grid(p, l, li.n_tasks);
       li.block = l.kernel == K_POOL_STAGED ? kStagedThreads : 256;
+      if (l.kernel == K_POOL_STAGED) {
+        li.smem_bytes = (int32_t)pool_staged_smem(l.tile_planes, (int)(s.in.h * s.in.w), (int)(s.out.h * s.out.w),
+                                                  l.stages);
+        li.tile_planes = l.tile_planes;
+        li.stages = l.stages;
+      }
     }
     int64_t rd = s.in.numel() * 4;
     for (auto* v : {&s.pro, &s.epi})

@@ -250,7 +250,8 @@ __device__ __forceinline__ void sts_f32(uint32_t a, float v) {
 
 // The same wait with a suspend-time hint: the waiting thread sleeps until the phase completes
 // (or the hint expires) instead of spinning on try_wait -- a producer or an idle consumer warp
-// then takes no issue slots from the warps doing the work.
+// then takes no issue slots from the warps doing the work.  (The try_wait loop is the standard
+// PTX idiom, as in CUTLASS cutlass/arch/barrier.h, BSD-3-Clause, NVIDIA.)
 #ifndef BS_MBAR_SLEEP_NS
 #define BS_MBAR_SLEEP_NS 0x989680
 #endif
@@ -315,6 +316,9 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* b) {
 // lets the next kernel start its launch as early as possible.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// One-time (per kernel, device) shared-memory attributes of the smem kernels (k_dispatch.cu).
+cudaError_t smem_kernel_setup(const void* fn);
 
 // Launch with the PDL attribute (see pdl_wait).
 cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st);

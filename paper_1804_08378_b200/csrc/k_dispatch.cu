@@ -23,27 +23,40 @@ static void* pool_fn(int kind, const PoolArgs& a) {
   return kind == K_POOL_STAGED ? pool_fn_staged(a) : pool_fn_global(kind, a);
 }
 
-// The shared-memory kernels (staged pools, sequences) all ask for the maximum shared-memory
-// carveout: an SM whose L1/shared split must change between two kernels has to drain first,
-// which defeats the PDL overlap of consecutive stacks needing different amounts of shared memory
-// (AlexNet step 46.1 -> 44.4 us).  The L1-streaming kernels keep the default split (forcing it
-// on them too cost DenseNet-121 17 %).
-void prefer_max_shared(const void* fn) {
-#ifndef BS_NO_CARVEOUT
+// The shared-memory kernels (staged pools, sequences) are configured ONCE per (kernel, device),
+// under a lock, before their first launch or occupancy query:
+//  * the dynamic shared-memory limit is raised to the device's opt-in maximum, never lowered
+//    -- so plans needing different amounts can launch the same instantiation from several host
+//    threads without a set-attribute / launch race (a launch uses only what it asks for);
+//  * the maximum shared-memory carveout: an SM whose L1/shared split must change between two
+//    kernels has to drain first, which defeats the PDL overlap of consecutive stacks needing
+//    different amounts of shared memory (AlexNet step 46.1 -> 44.4 us).  The L1-streaming
+//    kernels keep the default split (forcing it on them too cost DenseNet-121 17 %).
+cudaError_t smem_kernel_setup(const void* fn) {
   static std::mutex mu;
   static std::set<std::pair<const void*, int>> done;   // per (kernel, device)
   int dev = 0;
-  cudaGetDevice(&dev);
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lock(mu);
-  if (done.insert({fn, dev}).second)
-    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-#else
-  (void)fn;
+  if (done.count({fn, dev})) return cudaSuccess;
+  int optin = 0;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess) return e;
+#ifndef BS_NO_CARVEOUT
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
+    return e;
 #endif
+  done.insert({fn, dev});
+  return cudaSuccess;
 }
 
 cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
-  if (smem > 0) prefer_max_shared(fn);
+  if (smem > 0) {
+    const cudaError_t e = smem_kernel_setup(fn);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -68,8 +81,6 @@ cudaError_t launch_pool(const PoolArgs& a, int kind, int grid, int block, cudaSt
   void* args[] = {(void*)&a};
   if (kind == K_POOL_STAGED) {
     const size_t smem = pool_staged_smem(a.tile_planes, a.H * a.W, a.Ho * a.Wo, a.stages);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     return launch_pdl(fn, dim3(grid), dim3(kStagedThreads), args, smem, st);
   }
   return launch_pdl(fn, dim3(grid), dim3(kPoolBlock), args, 0, st);
@@ -83,7 +94,7 @@ int pool_max_blocks_per_sm(int kind, const PoolArgs& a, int block) {
   if (!fn) return 0;
   if (kind == K_POOL_STAGED) {
     const size_t smem = pool_staged_smem(a.tile_planes, a.H * a.W, a.Ho * a.Wo, a.stages);
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+    if (smem_kernel_setup(fn) != cudaSuccess) return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kStagedThreads, smem) != cudaSuccess) n = 0;
     return n;
   }

@@ -57,9 +57,11 @@ __global__ void __launch_bounds__(kPoolBlock) pool_cw_spec(PoolArgs a) {
             for (int q = 0; q < NR; ++q) v[q] = xorsign(v[q], flip);
           }
         } else if (PC != PC_NONE) {
+          // padding-column lanes (T.c outside the row) load a clamped column; they skip the
+          // program (an ADD operand would otherwise be read at T.c < 0) and are discarded below
           bool ok[NR];
 #pragma unroll
-          for (int q = 0; q < NR; ++q) ok[q] = true;
+          for (int q = 0; q < NR; ++q) ok[q] = T.col_ok;
           apply_rows<PC, NR>(a.pro, paff, ch, v, ok, ident, in_idx0 + (int64_t)r0 * a.W, a.W);
         }
         char* po = (char*)pout + (size_t)((unsigned)i * Wo4);

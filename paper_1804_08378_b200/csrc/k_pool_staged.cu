@@ -106,26 +106,28 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   }
 
   // ---------------- consumers
-  // Each warp owns the same <= 2 items of every tile (it = cw, cw + 8; the planner keeps
-  // I <= 16), so the item geometry is decoded once, outside the tile loop.
+  // Warp cw walks items cw, cw + 8, cw + 16, ... of every tile.  The planner keeps I <= 16
+  // where it can, so the geometry of a warp's first two items is decoded once, outside the
+  // tile loop; items beyond those (very wide planes, Wo > 16 * 32, or forced narrow column
+  // groups) are decoded per tile.
   const int cw = warp - 1;
   const int J = a.Jg;                 // output columns per lane group (G groups per warp)
   const int g = lane / J, l = lane - g * J;
   const int items = ((P + a.G - 1) / a.G) * a.n_cc * a.n_rb;
-  int it_pin[2], it_j[2], it_i0[2], it_i1[2];
-  bool it_ok[2];
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int it = cw + q * kStagedConsumerWarps;
+  struct Item { int pin, j, i0, i1; bool ok; };
+  auto decode = [&](int it) -> Item {
+    Item r;
     const int rb = it % a.n_rb;
     const int rest = it / a.n_rb;
     const int cc = rest % a.n_cc;
-    it_pin[q] = (rest / a.n_cc) * a.G + g;
-    it_j[q] = cc * J + l;
-    it_i0[q] = rb * a.rows_per_task;
-    it_i1[q] = min(a.Ho, it_i0[q] + a.rows_per_task);
-    it_ok[q] = it < items && g < a.G && l < J && it_j[q] < a.Wo;
-  }
+    r.pin = (rest / a.n_cc) * a.G + g;
+    r.j = cc * J + l;
+    r.i0 = rb * a.rows_per_task;
+    r.i1 = min(a.Ho, r.i0 + a.rows_per_task);
+    r.ok = it < items && g < a.G && l < J && r.j < a.Wo;
+    return r;
+  };
+  const Item it0 = decode(cw), it1 = decode(cw + kStagedConsumerWarps);
   const float ident = IS_MAX ? -CUDART_INF_F : 0.f;
   constexpr int CARRY = KH > SH ? KH - SH : 0;
   constexpr int NEW = KH - CARRY;
@@ -144,10 +146,11 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
 #ifdef BS_DBG_NOCOMPUTE
     if (items < 0)
 #endif
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (!it_ok[q] || it_pin[q] >= np) continue;
-      const int pin = it_pin[q], j = it_j[q], i0 = it_i0[q], i1 = it_i1[q];
+#pragma unroll 1
+    for (int it = cw; it < items; it += kStagedConsumerWarps) {
+      const Item I = it == cw ? it0 : it == cw + kStagedConsumerWarps ? it1 : decode(it);
+      if (!I.ok || I.pin >= np) continue;
+      const int pin = I.pin, j = I.j, i0 = I.i0, i1 = I.i1;
       const uint32_t plane = (uint32_t)(a.plane0 + p0 + pin);
       const int ch = (int)(plane - fdiv(plane, a.cdiv) * (uint32_t)a.C);
       float2 paff[kAffSlots], eaff[kAffSlots];

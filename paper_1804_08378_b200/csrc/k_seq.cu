@@ -255,16 +255,13 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
 cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st) {
   void* args[] = {(void*)&a};
   const size_t smem = seq_smem(a);
-  cudaError_t e = cudaFuncSetAttribute((void*)seq_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   return launch_pdl((void*)seq_staged, dim3(grid), dim3(kSeqThreads), args, smem, st);
 }
 
 int seq_max_blocks_per_sm(const SeqArgs& a) {
   const size_t smem = seq_smem(a);
   int n = 0;
-  if (cudaFuncSetAttribute((void*)seq_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return 0;
+  if (smem_kernel_setup((const void*)seq_staged) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, (void*)seq_staged, kSeqThreads, smem) != cudaSuccess) n = 0;
   return n;
 }

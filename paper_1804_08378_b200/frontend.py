@@ -148,15 +148,42 @@ class Stack:
         return "[" + ",".join(L.kind for L in self.layers) + "]"
 
 
+def _meta(n) -> Optional[object]:
+    return n.meta.get("tensor_meta") if isinstance(n, fx.Node) else None
+
+
+def _shape_ok(spec: LayerSpec, n: fx.Node, x: fx.Node, opnd: Optional[fx.Node]) -> bool:
+    """With shape metadata (ShapeProp over an example input): the data input must be a float32
+    tensor (4-D for anything but a flat element-wise layer), and an ADD must be a same-shape,
+    same-dtype residual add -- a broadcasting add stays in PyTorch."""
+    mx, mn = _meta(x), _meta(n)
+    if mx is None or mn is None:   # ShapeProp records tensor_meta for tensor values only
+        return False
+    if not hasattr(mx, "shape") or mx.dtype != torch.float32:
+        return False
+    if len(mx.shape) != 4 and spec.kind not in ("relu", "copy", "scale", "add"):
+        return False
+    if spec.kind == "add":
+        mo = _meta(opnd)
+        return (mo is not None and hasattr(mo, "shape") and mo.dtype == torch.float32
+                and tuple(mo.shape) == tuple(mx.shape) == tuple(mn.shape))
+    return True
+
+
 def find_stacks(gm: fx.GraphModule) -> List[Stack]:
-    """Group the optimizable nodes of `gm`'s graph into stacks (SURVEY.md Appendix A rule)."""
+    """Group the optimizable nodes of `gm`'s graph into stacks (SURVEY.md Appendix A rule).
+    When the graph carries shape metadata (``optimize(model, example_input)``), only float32
+    tensor nodes are classified and ADDs must be same-shape residual adds."""
     stacks: List[Stack] = []
     cur: Optional[Stack] = None
+    has_meta = any("tensor_meta" in n.meta for n in gm.graph.nodes)
     for n in gm.graph.nodes:
         c = _classify(gm, n)
         if c is None:
             continue
         spec, x, opnd = c
+        if has_meta and not _shape_ok(spec, n, x, opnd):
+            continue
         if spec.kind == "add":
             # the summand that continues the current stack is the data input, the other an operand
             a, b = x, opnd
@@ -212,7 +239,60 @@ class BrainSlugStack(nn.Module):
             out.append(L)
         return out
 
+    def _scalar_forward(self, x, operands):
+        """A stack classified from the graph alone can receive Python numbers (e.g. ``x.shape[2] * 2``
+        traced without example inputs): evaluate it with plain Python semantics -- this is graph
+        bookkeeping, not tensor work, and nothing of a tensor runs here."""
+        for L in self.layers:
+            if L.kind == "relu":
+                x = x if x > 0 else 0 * x
+            elif L.kind == "copy":
+                pass
+            elif L.kind == "scale":
+                x = x * L.alpha
+            elif L.kind == "add":
+                x = x + operands[L.operand - 1]
+            else:
+                raise TypeError(f"BrainSlugStack {self.name}: a {L.kind} layer needs a tensor, got {type(x)}")
+        return x
+
+    def _check_operands(self, x: torch.Tensor, operands) -> List[torch.Tensor]:
+        """Each ADD operand must have the shape of the tensor at its layer (the C ABI reads exactly
+        that many elements): broadcastable operands are expanded, anything else is an error."""
+        shape = tuple(x.shape)
+        N, C, H, W = shape
+        want = {}
+        for L in self.layers:
+            if L.kind == "add":
+                want[L.operand] = (N, C, H, W)
+            elif L.kind in ("maxpool", "avgpool") and not L.global_pool:
+                (kh, kw), (sh, sw), (ph, pw) = L.kernel, L.stride, L.padding
+                H, W = (H + 2 * ph - kh) // sh + 1, (W + 2 * pw - kw) // sw + 1
+            elif L.kind in ("maxpool", "avgpool"):
+                H, W = 1, 1
+        out = []
+        for k, o in enumerate(operands, start=1):
+            if not isinstance(o, torch.Tensor):
+                o = torch.as_tensor(o, dtype=torch.float32, device=x.device)
+            if o.device != x.device or o.dtype != torch.float32:
+                raise RuntimeError(f"BrainSlugStack {self.name}: ADD operand {k} is {o.dtype} on {o.device}; "
+                                   f"needs float32 on {x.device}")
+            exp = want[k]
+            if tuple(o.shape) != exp:
+                try:
+                    ok = tuple(torch.broadcast_shapes(tuple(o.shape), exp)) == exp
+                except RuntimeError:
+                    ok = False
+                if not ok:
+                    raise RuntimeError(f"BrainSlugStack {self.name}: ADD operand {k} of shape {tuple(o.shape)} "
+                                       f"does not broadcast to the stack tensor {exp} at that layer")
+                o = o.expand(exp)
+            out.append(o.contiguous())
+        return out
+
     def forward(self, x: torch.Tensor, *operands: torch.Tensor) -> torch.Tensor:
+        if not isinstance(x, torch.Tensor):
+            return self._scalar_forward(x, operands)
         if not x.is_cuda:
             raise RuntimeError(f"BrainSlugStack {self.name}: input on {x.device}; the stack runs only on "
                                "CUDA (sm_100a kernels) -- there is no CPU fallback")
@@ -223,10 +303,17 @@ class BrainSlugStack(nn.Module):
         if flat:   # element-wise stack on a non-image tensor (e.g. a classifier's ReLU/Dropout)
             shape = x.shape
             flat4 = (1, 1, 1, x.numel()) if x.numel() else (0, 1, 1, 1)   # empty: an empty batch
+            for k, o in enumerate(operands, start=1):
+                if not isinstance(o, torch.Tensor) or o.dtype != torch.float32 or o.device != x.device:
+                    raise RuntimeError(f"BrainSlugStack {self.name}: ADD operand {k} must be a float32 "
+                                       f"tensor on {x.device}")
+                if tuple(torch.broadcast_shapes(tuple(o.shape), tuple(shape))) != tuple(shape):
+                    raise RuntimeError(f"BrainSlugStack {self.name}: ADD operand {k} of shape "
+                                       f"{tuple(o.shape)} does not broadcast to {tuple(shape)}")
             y = self.forward(x.reshape(flat4), *[o.expand(shape).reshape(flat4) for o in operands])
             return y.reshape(shape)
         x = x.contiguous()
-        ops = [o.contiguous() for o in operands]
+        ops = self._check_operands(x, operands)
         key = (tuple(x.shape), x.device.index)
         entry = self._plans.get(key)
         if entry is None:
@@ -241,13 +328,20 @@ class BrainSlugStack(nn.Module):
         return self.signature()
 
 
-def optimize(model: nn.Module, min_layers: int = 1) -> fx.GraphModule:
+def optimize(model: nn.Module, min_layers: int = 1, example_input: Optional[torch.Tensor] = None) -> fx.GraphModule:
     """``brainslug.optimize(model)`` (lst:python P:L531-543): the model with every stack of
     >= `min_layers` optimizable layers replaced by a BrainSlugStack.  `model` must be in eval
-    mode (inference BatchNorm / Dropout); the result runs on CUDA."""
+    mode (inference BatchNorm / Dropout); the result runs on CUDA.  With `example_input` the
+    graph is shape-propagated first (torch.fx ShapeProp, on that tensor's device) and only
+    float32 tensor nodes / same-shape residual adds join stacks; without it, classification is
+    structural and each stack checks its operands at run time."""
     if model.training:
         raise ValueError("optimize() needs an eval-mode model (inference BatchNorm and Dropout)")
     gm = model if isinstance(model, fx.GraphModule) else fx.symbolic_trace(model)
+    if example_input is not None:
+        from torch.fx.passes.shape_prop import ShapeProp
+        with torch.no_grad():
+            ShapeProp(gm).propagate(example_input)
     stacks = find_stacks(gm)
     replaced: Dict[fx.Node, fx.Node] = {}   # tail of an already replaced stack -> its new node
     for i, st in enumerate(stacks):

@@ -64,6 +64,35 @@ def uniform_np(seed: int, count: int, start: int = 0) -> np.ndarray:
     return ((k - (1 << 23)).astype(np.float64) * 2.0 ** -23).astype(np.float32)
 
 
+VARIANTS = ("uniform", "allneg", "ties", "const", "signed_zero")
+
+
+def variant_np(kind: str, seed: int, count: int, start: int = 0) -> np.ndarray:
+    """Correctness-only input variants (SURVEY.md §8(d) "Correctness-only variants"), built from
+    the same stream; no arithmetic of the method:
+      uniform     : the default k*2^-23 in [-1, 1)
+      allneg      : u - 1 in [-2, 0) (exact: |k - 2^23| < 2^24), every element < 0
+      ties        : round(4u)/4 in {-1, -0.75, ..., 1}, +0.0 for zeros (many equal window values)
+      const       : one value (0.375 + u_0/4, u_0 the first draw) everywhere
+      signed_zero : +0.0 / -0.0 chosen by a draw bit, a quarter of the elements a small negative
+                    value (so window maxima are mostly zeros of either sign)"""
+    u = uniform_np(seed, count, start)
+    if kind == "uniform":
+        return u
+    if kind == "allneg":
+        return (u.astype(np.float64) - 1.0).astype(np.float32)
+    if kind == "ties":
+        return (np.round(4.0 * u.astype(np.float64)) / 4.0 + 0.0).astype(np.float32)
+    if kind == "const":
+        return np.full(count, np.float32(0.375 + uniform_np(seed, 1)[0] / 4.0), dtype=np.float32)
+    if kind == "signed_zero":
+        d = splitmix64_np(seed, start, count)
+        z = np.where((d & np.uint64(1)) == 0, np.float32(0.0), np.float32(-0.0))
+        neg = (d >> np.uint64(1)) & np.uint64(3) == 0
+        return np.where(neg, -np.abs(u) - np.float32(2.0 ** -20), z).astype(np.float32)
+    raise ValueError(f"unknown variant {kind!r}")
+
+
 def _as_signed(v: int) -> int:
     v &= _M64
     return v - (1 << 64) if v >= (1 << 63) else v

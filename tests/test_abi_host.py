@@ -279,3 +279,21 @@ def test_smem_budget_option(bs):
     assert bs.bs_plan_query_launch(host_plan(bs, s1.layers, s1.shape), 0)["kernel"] == 6
     p = bs.bs_plan_create(s1.layers, s1.shape, {"host_only": 1, "smem_budget_bytes": 40 * 1024})
     assert bs.bs_plan_query_launch(p, 0)["kernel"] == 2      # 2 x 24 KB stages do not fit 40 KB
+
+
+@pytest.mark.parametrize("shape,layers", [
+    ((1, 1, 3, 7999), [synth.relu(), synth.maxpool(3, 2)]),
+    ((1, 1, 9, 2049), [synth.maxpool(3, 1, 1)]),
+    ((1, 2, 11, 1501), [synth.relu(), synth.maxpool(3, 2, 1)]),
+    ((1, 1, 8, 1030), [synth.maxpool(3, 1, 1)]),
+])
+def test_wide_plane_plans(bs, shape, layers):
+    """Planes wider than 16 column chunks: the staged kernel walks every item
+    of a tile (any count), and the launch info reports the ring it runs with."""
+    p = host_plan(bs, layers, shape, force_generic=3)
+    li = bs.bs_plan_query_launch(p, 0)
+    assert li["kernel_name"] == "pool_staged_tma"
+    Wo = bs.bs_plan_query(p)["out"][3]
+    assert li["outputs_per_group"] * -(-Wo // li["outputs_per_group"]) >= Wo
+    assert li["tile_planes"] >= 1 and li["stages"] >= 2
+    assert li["smem_bytes"] >= 128 + li["stages"] * li["tile_planes"] * shape[2] * shape[3] * 4

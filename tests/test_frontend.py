@@ -164,3 +164,68 @@ def test_mixed_model_matches_eager(cuda_dev):
         ref = m(x)
         got = fe.optimize(m)(x)
     assert torch.allclose(got, ref, rtol=1e-4, atol=1e-5), (got - ref).abs().max().item()
+
+
+class _BroadcastAdd(torch.nn.Module):
+    """relu(conv(x)) + b with b of shape (1, C, 1, 1): not a same-shape residual add."""
+
+    def __init__(self):
+        super().__init__()
+        self.conv = torch.nn.Conv2d(3, 4, 1)
+        self.b = torch.nn.Parameter(torch.arange(4.0).reshape(1, 4, 1, 1))
+
+    def forward(self, x):
+        return torch.relu(self.conv(x)) + self.b
+
+
+class _ShapeArith(torch.nn.Module):
+    """x.shape[2] * 2 is a Python int in eager mode; a stack must not break it."""
+
+    def forward(self, x):
+        k = x.shape[2] * 2
+        return torch.relu(x) * 1.0 + k
+
+
+def test_broadcast_add_excluded_with_example_input():
+    from paper_1804_08378_b200 import frontend as fe
+    m = _BroadcastAdd().eval()
+    gm = fe.optimize(m, example_input=torch.zeros(2, 3, 5, 5))
+    sig = [mod.signature() for mod in gm.modules() if isinstance(mod, fe.BrainSlugStack)]
+    assert sig == ["[relu]"]          # the broadcasting add stays in PyTorch
+
+
+def test_shape_arithmetic_excluded_with_example_input():
+    from paper_1804_08378_b200 import frontend as fe
+    gm = fe.optimize(_ShapeArith().eval(), example_input=torch.zeros(1, 2, 3, 3))
+    sig = [mod.signature() for mod in gm.modules() if isinstance(mod, fe.BrainSlugStack)]
+    assert sig == ["[relu,scale]"]    # int arithmetic and the tensor + int add stay in PyTorch
+
+
+def test_scalar_stack_runs_python_semantics():
+    """Without shape metadata, `x.shape[2] * 2` may be classified; it must still compute an int."""
+    from paper_1804_08378_b200 import frontend as fe
+    st = fe.BrainSlugStack([fe.LayerSpec("scale", alpha=2.0)], "s")
+    assert st(7) == 14.0
+
+
+@pytest.mark.gpu
+def test_broadcast_add_operand_checked_at_run_time(cuda_dev):
+    """Structural classification (no example input) turns the broadcasting add into a stack: the
+    stack expands the (1, C, 1, 1) operand to the tensor's shape instead of reading past it."""
+    from paper_1804_08378_b200 import frontend as fe
+    torch.manual_seed(5)
+    m = _BroadcastAdd().eval().cuda()
+    x = torch.randn(2, 3, 5, 5, device="cuda")
+    with torch.no_grad():
+        ref = m(x)
+        gm = fe.optimize(m)
+        assert any(mod.signature() == "[relu,add]" for mod in gm.modules() if isinstance(mod, fe.BrainSlugStack))
+        got = gm(x)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    st = fe.BrainSlugStack([fe.LayerSpec("relu"), fe.LayerSpec("add", operand=1)], "bad")
+    with pytest.raises(RuntimeError, match="does not broadcast"):
+        st(x, torch.zeros(3, 1, 1, device="cuda"))
+    with torch.no_grad():   # shape arithmetic stays an int through a classified stack
+        gm2 = fe.optimize(_ShapeArith().eval())
+        assert torch.equal(gm2(x), _ShapeArith()(x))

@@ -39,3 +39,21 @@ def test_workload_shapes():
     assert sum(c.count for c in r) == 33
     d = synth.workload("densenet121")
     assert len(d) == 121
+
+
+def test_variants():
+    n = 1 << 14
+    a = synth.variant_np("allneg", 3, n)
+    assert np.all(a < 0) and a.min() >= -2.0
+    assert np.array_equal(a.astype(np.float64), synth.uniform_np(3, n).astype(np.float64) - 1.0)
+    t = synth.variant_np("ties", 3, n)
+    assert set(np.unique(t).tolist()) <= {q / 4 for q in range(-4, 5)}
+    assert not np.any(np.signbit(t) & (t == 0))
+    c = synth.variant_np("const", 3, n)
+    assert np.all(c == c[0])
+    z = synth.variant_np("signed_zero", 3, n)
+    zero = z == 0
+    assert 0.6 < zero.mean() < 0.9
+    assert 0.2 < np.signbit(z[zero]).mean() < 0.8      # both zero signs present
+    assert np.all(z[~zero] < 0)
+    assert np.array_equal(synth.variant_np("uniform", 3, n), synth.uniform_np(3, n))
