@@ -2,24 +2,35 @@
 """Benchmark of the depth-first stack executor on BASELINE.json's metric.
 
 metric : "fused-stack HBM GB/s (% of B200 peak) and images/sec at 1/2/4/8 GPUs"
-value  : whole-job images/s (all ranks) for one pass of every stack of the workload over
-         one batch per rank ("step"); GB/s and % of the measured HBM peak ride alongside.
-default workload: configs[1], AlexNet's three ReLU->MaxPool3x3/s2 stacks at batch 128
-         (`--workload vgg16|resnet50|densenet121|c1` selects the other configs).
+value  : whole-job images/s (all ranks) for one pass of every stack of the workload over one
+         batch per rank (a "step"); GB/s and % of the measured HBM peak ride alongside.
+default workload: configs[3], ResNet-50's stem BN->ReLU->MaxPool3x3/s2/p1 + 32 BN->ReLU stacks
+         at batch 256 -- the largest BASELINE config that runs on one GPU (7.76 GB per step).
+         The same run also measures configs[1] AlexNet, configs[2] VGG-16 and configs[4]
+         DenseNet-121 ("workloads" key; `--no-extra` skips them) and configs[0] C1 ("c1" key:
+         the GPU time and the CPU oracle's time in ms, min of 5 runs).
 
-Multi-GPU (torchrun, one process per GPU): every rank runs its own batch (weak scaling,
-the batch dimension is the unit that shards); no collective on the data path.  NCCL is
-used only after the timed region: max-over-ranks time and per-rank output checksums.
+Multi-GPU (torchrun, one process per GPU): the batch dimension is the unit that shards (every
+image is independent).  ResNet-50 / AlexNet / VGG-16 run weak-scaled (every rank
+its BASELINE batch); DenseNet-121 is strong-scaled by default (BASELINE.json: its batch 256
+"sharded across 8xB200").  No collective on the data path: NCCL only after the timed region
+(max-over-ranks times, per-rank checksums, and an all-gather of the dominant stack's output
+shards, sampled images compared with the CPU oracle on rank 0).  The aggregate images/s uses
+the slower of (max over ranks of the CUDA-event time) and (max over ranks of the host
+wall-clock between the barriers that bracket the timed region), so ranks sharing one GPU cannot
+report more than that GPU delivers.
 
-Timing: W warm-up steps, then K steps between barrier + cuda.synchronize on both sides,
-CUDA events on the launching stream; inputs rotate over enough buffer sets to exceed
-4x the L2 (or are larger than L2).  The dominant kernel is timed with events around its
-own launches for the roofline object.  `--impl reference` times the CPU oracle instead
+Timing: W warm-up steps, then K steps between barrier + cuda.synchronize on both sides, CUDA
+events on the launching stream; inputs rotate over enough buffer sets to exceed 4x the L2 (or
+are larger than L2).  The dominant kernel is timed alone (events around back-to-back launches)
+for the roofline object; every stack is also timed alone against a same-size ideal streaming
+kernel (benchlib/ceiling.cu) -- "per_stack".  `--impl reference` times the CPU oracle instead
 (rank 0 only), a bounded sample of images per step.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
@@ -37,6 +48,8 @@ import synth  # noqa: E402
 METRIC = "fused-stack HBM GB/s (% of B200 peak) and images/sec at 1/2/4/8 GPUs"
 CONFIG_INDEX = {"c1": 0, "alexnet": 1, "vgg16": 2, "resnet50": 3, "densenet121": 4,
                 "resnet50_residual": None}   # NEXT-1: not a BASELINE config
+STRONG_BY_DEFAULT = {"densenet121"}          # BASELINE.json configs[4]: "sharded across 8xB200"
+EXTRA_WORKLOADS = ("alexnet", "vgg16", "densenet121")
 
 
 def load_peaks():
@@ -52,6 +65,15 @@ def instances(cases):
     for c in cases:
         out += [c] * c.count
     return out
+
+
+def kernel_sources_hash() -> str:
+    """sha256 (16 hex) of the kernel + planner sources: keys stored ncu traffic to the build."""
+    import glob
+    h = hashlib.sha256()
+    for p in sorted(glob.glob(os.path.join(ROOT, "paper_1804_08378_b200", "csrc", "*"))):
+        h.update(open(p, "rb").read())
+    return h.hexdigest()[:16]
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -109,6 +131,47 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# ----------------------------------------------------------------------------- multi-rank host logic
+# (no CUDA here: tests/test_bench_dist.py drives these under torchrun + gloo with a stub executor)
+def shard_of(n_total: int, world: int, rank: int, strong: bool):
+    """(lo, hi) global image range of `rank`: strong = n_total split over the ranks, weak = every
+    rank its own n_total images (the global batch is world * n_total)."""
+    from paper_1804_08378_b200 import dist as bsd
+    if strong:
+        return bsd.shard(n_total, world, rank)
+    return rank * n_total, (rank + 1) * n_total
+
+
+def aggregate(images_local: int, event_ms_local: float, wall_s_local: float, steps: int, device="cpu"):
+    """Whole-job rate of a timed region bracketed by barriers on every rank.  The job time is the
+    slower of the max-over-ranks device time and the max-over-ranks host wall-clock between the
+    barriers: ranks whose work does not really overlap (several ranks on one GPU) cannot add up
+    to more than the device delivers."""
+    from paper_1804_08378_b200 import dist as bsd
+    g = bsd.gather_stats([float(images_local), float(event_ms_local), float(wall_s_local)], device)
+    images = int(round(sum(r[0] for r in g)))
+    ev_max = max(r[1] for r in g)
+    wall_max = max(r[2] for r in g)
+    t_s = max(ev_max / 1e3, wall_max)
+    return {"images_per_step": images, "event_ms_max": ev_max, "wall_s_max": wall_max,
+            "time_s": t_s, "ms_per_step": 1e3 * t_s / steps, "images_per_s": images * steps / t_s,
+            "timer": "wall" if wall_max >= ev_max / 1e3 else "events",
+            "per_rank": [{"images": int(r[0]), "event_ms": r[1], "wall_s": r[2]} for r in g]}
+
+
+def validate_gathered(gathered, n_total: int, ref_image, check, samples=3):
+    """Compare sampled global images of an all-gathered output with a reference (the oracle).
+    ref_image(n) -> expected output of image n (1, C, Ho, Wo); check(got, ref, ctx) raises."""
+    idx = sorted({0, n_total // 2, n_total - 1} | {int(v) for v in np.linspace(0, n_total - 1, samples)})
+    errs = []
+    for n in idx:
+        try:
+            check(np.asarray(gathered[n:n + 1]), ref_image(n), f"image {n}")
+        except AssertionError as e:
+            errs.append(str(e)[:200])
+    return {"images_checked": idx, "ok": not errs, "errors": errs}
+
+
 # ----------------------------------------------------------------------------- CPU oracle timing
 def _cpu_model() -> str:
     try:
@@ -120,16 +183,22 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+def _oracle_image(case, k):
+    shp = (1,) + tuple(case.shape[1:])
+    n = int(np.prod(shp))
+    x = synth.uniform_np(case.input_seed, n, start=k * n).reshape(shp)
+    ops = [synth.uniform_np(sd, n, start=k * n).reshape(shp) for sd in case.operand_seeds]
+    return x, ops
+
+
 def time_oracle(cases, budget_s: float, max_images: int):
     """The oracle as it stands (single thread) on whole images of the workload."""
     import oracle
     oracle.build()
+
     def one_image(k):
         for c in cases:
-            shp = (1,) + tuple(c.shape[1:])
-            x = synth.uniform_np(c.input_seed, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
-            ops = [synth.uniform_np(sd, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
-                   for sd in c.operand_seeds]
+            x, ops = _oracle_image(c, k)
             for _ in range(c.count):
                 oracle.run_bf(c.layers, x, ops)
     t0 = time.perf_counter()
@@ -143,6 +212,20 @@ def time_oracle(cases, budget_s: float, max_images: int):
     return n / T, n, T
 
 
+def c1_oracle_ms(reps: int = 5) -> float:
+    """BASELINE.json configs[0] on the CPU oracle, in ms: min of `reps` runs."""
+    import oracle
+    oracle.build()
+    case = synth.workload("c1")[0]
+    x = synth.uniform_np(case.input_seed, int(np.prod(case.shape))).reshape(case.shape)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.run_bf(case.layers, x)
+        ts.append(time.perf_counter() - t0)
+    return 1e3 * min(ts)
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed on the host cores, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
@@ -151,12 +234,10 @@ def run_reference(args):
     cases = synth.workload(args.workload, batch=1)
     import oracle
     oracle.build()
+
     def step(k):
         for c in cases:
-            shp = (1,) + tuple(c.shape[1:])
-            x = synth.uniform_np(c.input_seed, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
-            ops = [synth.uniform_np(sd, int(np.prod(shp)), start=k * int(np.prod(shp))).reshape(shp)
-                   for sd in c.operand_seeds]
+            x, ops = _oracle_image(c, k)
             for _ in range(c.count):
                 oracle.run_bf(c.layers, x, ops)
     for k in range(args.warmup):
@@ -169,8 +250,8 @@ def run_reference(args):
     batch = synth.DEFAULT_BATCH[args.workload]
     line = {"impl": "reference", "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 arithmetic, f32 tensors",
-            "data": "synthetic (SplitMix64, seeded)",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 arithmetic, f32 tensors", "data": "synthetic (SplitMix64, seeded)",
             "config": {"workload": args.workload, "baseline_config_index": CONFIG_INDEX[args.workload],
                        "global_batch": batch, "parallelism": "none (host CPU oracle)"},
             "cpu_baseline": {"value": ips, "unit": "images/s", "cores": 1, "kind": "oracle",
@@ -181,239 +262,316 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU bench
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--impl", default="brainslug", choices=["brainslug", "reference"])
-    ap.add_argument("--workload", default="alexnet", choices=list(CONFIG_INDEX))
-    ap.add_argument("--batch", type=int, default=0, help="per-rank batch (0 = BASELINE.json batch)")
-    ap.add_argument("--e2e-steps", type=int, default=0)
-    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work for cpu_baseline")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-lbl", action="store_true", help="skip the torch layer-by-layer context number")
-    ap.add_argument("--out", default="", help="also append the JSON line to this file")
-    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of CUDA graph replays")
-    ap.add_argument("--per-stack", action="store_true", help="add a per-stack timing breakdown")
-    ap.add_argument("--strong", action="store_true", help="split the BASELINE batch over ranks (strong scaling)")
-    args = ap.parse_args()
-    args.warmup = max(3, args.warmup)
-    if args.impl == "reference":
-        return run_reference(args)
+class Ctx:
+    """Process-wide state of a GPU run."""
 
-    import torch
-    import torch.distributed as dist
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.args = torch, dist, args
+        import paper_1804_08378_b200 as bs
+        self.bs = bs
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # one process per GPU; BS_BENCH_BACKEND=gloo lets several ranks share one GPU (testing the
+        # multi-rank path on a 1-GPU box)
+        self.backend = os.environ.get("BS_BENCH_BACKEND", "nccl")
+        dev_idx = self.local % torch.cuda.device_count()
+        torch.cuda.set_device(dev_idx)
+        self.dev = torch.device("cuda", dev_idx)
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group(self.backend)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.sh = self.stream.cuda_stream
+        self.l2 = torch.cuda.get_device_properties(self.dev).L2_cache_size
+        self.peak, self.peak_src = load_peaks()
 
-    import paper_1804_08378_b200 as bs
-    from paper_1804_08378_b200 import dist as bsd
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # one process per GPU; BS_BENCH_BACKEND=gloo lets several ranks share one GPU (testing the
-    # multi-rank path on a 1-GPU box)
-    backend = os.environ.get("BS_BENCH_BACKEND", "nccl")
-    local_dev = local % torch.cuda.device_count()
-    torch.cuda.set_device(local_dev)
-    dev = torch.device("cuda", local_dev)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
+    def event(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def launch(self, h, xs, y):
+        if len(xs) == 1:
+            self.bs.bs_execute(h, xs[0].data_ptr(), y.data_ptr(), self.sh)
         else:
-            dist.init_process_group(backend)
+            self.bs.bs_execute_ex(h, [t.data_ptr() for t in xs], y.data_ptr(), self.sh)
 
-    full_batch = args.batch or synth.DEFAULT_BATCH[args.workload]
-    if args.strong:   # strong scaling: the BASELINE batch is split over the ranks
-        lo, hi = bsd.shard(full_batch, world, rank)
-        batch = hi - lo
-    else:             # weak scaling: every rank runs the BASELINE batch
-        batch = full_batch
-    cases = synth.workload(args.workload, batch=batch)
+    def burst_ms(self, fn, reps=3):
+        """Average time of fn() (one burst) captured once as a torch CUDA graph, over `reps` replays."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            fn()
+        torch.cuda.synchronize()
+        a, b = self.event(), self.event()
+        with torch.cuda.stream(self.stream):
+            g.replay()
+            a.record(self.stream)
+            for _ in range(reps):
+                g.replay()
+            b.record(self.stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        del g
+        return ms
+
+
+def stack_burst(ctx, case, plan, nb, extra_seed):
+    """Rotating buffer sets of one stack (> 4x L2 in total) for burst timing."""
+    torch = ctx.torch
+    nset = min(64, int(math.ceil(4 * ctx.l2 / nb)) + 1)
+    sb = [([synth.uniform_torch(sd + extra_seed * q, case.shape, device=ctx.dev)
+            for sd in [case.input_seed] + case.operand_seeds],
+           torch.empty(ctx.bs.bs_plan_query(plan)["out"], device=ctx.dev)) for q in range(nset)]
+    R = max(8, min(64, 2 * nset))
+    return sb, R
+
+
+def measure_stack_alone(ctx, case, plan, info):
+    """One stack alone: R back-to-back launches over rotating buffers (one CUDA graph), and the
+    same-size ideal streaming kernel (fastest of benchlib.VARIANTS) on the same byte counts."""
+    import benchlib
+    nb = info["alg_bytes_read"] + info["alg_bytes_written"]
+    sb, R = stack_burst(ctx, case, plan, nb, 13)
+
+    def burst():
+        for r in range(R):
+            xs, y = sb[r % len(sb)]
+            ctx.launch(plan, xs, y)
+    t = ctx.burst_ms(burst) / R
+    n_in = info["alg_bytes_read"] // 4
+    n_out = info["alg_bytes_written"] // 4
+    cin = [ctx.torch.empty(n_in, device=ctx.dev) for _ in range(len(sb))]
+    cout = [y.view(-1) for _, y in sb]
+    best = None
+    for v in benchlib.VARIANTS:
+        def cburst(v=v):
+            for r in range(R):
+                benchlib.launch(v, cin[r % len(sb)].data_ptr(), n_in, cout[r % len(sb)].data_ptr(), n_out, ctx.sh)
+        tc = ctx.burst_ms(cburst) / R
+        if best is None or tc < best[0]:
+            best = (tc, v)
+    del sb, cin, cout
+    gbs = nb / (t / 1e3) / 1e9
+    return {"stack": case.name, "count": case.count, "shape": list(case.shape), "ms": t, "gbs": gbs,
+            "frac_of_copy": gbs / ctx.peak, "ceiling_ms": best[0], "ceiling_variant": "/".join(map(str, best[1])),
+            "frac_of_ceiling": best[0] / t,
+            "kernel": ctx.bs.KERNEL_NAMES[ctx.bs.bs_plan_query_launch(plan, 0)["kernel"]]}
+
+
+def measure(ctx, wl: str, full: bool):
+    """Time workload `wl` (one step = every stack of the network once over one batch per rank)."""
+    torch, bs, args = ctx.torch, ctx.bs, ctx.args
+    full_batch = args.batch or synth.DEFAULT_BATCH[wl]
+    strong = args.strong or (wl in STRONG_BY_DEFAULT and not args.weak)
+    lo, hi = shard_of(full_batch, ctx.world, ctx.rank, strong)
+    batch = hi - lo
+    n_total = full_batch if strong else full_batch * ctx.world
+    cases = synth.workload(wl, batch=batch)
     inst = instances(cases)
-    plans = {}
-    for c in cases:
-        plans[c.name] = bs.bs_plan_create(c.layers, c.shape)
+    plans = {c.name: bs.bs_plan_create(c.layers, c.shape) for c in cases}
     infos = {c.name: bs.bs_plan_query(plans[c.name]) for c in cases}
     launches_per_step = sum(infos[c.name]["n_launches"] for c in inst)
     step_bytes = sum(infos[c.name]["alg_bytes_read"] + infos[c.name]["alg_bytes_written"] for c in inst)
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    n_sets = 1 if step_bytes >= 8 * l2 else int(math.ceil(4 * l2 / step_bytes)) + 1
-    # buffers: per instance per set (inputs distinct per instance so nothing is re-read from L2)
+    n_sets = 1 if step_bytes >= 8 * ctx.l2 else int(math.ceil(4 * ctx.l2 / step_bytes)) + 1
+    # buffers per instance per set; each rank's inputs are its slice [lo, hi) of the global
+    # image stream, so the gathered outputs are those of one global batch
     bufs = []
     for s in range(n_sets):
         row = []
         for j, c in enumerate(inst):
-            x = synth.uniform_torch(c.input_seed + 7 * j, c.shape, device=dev, start=rank * int(np.prod(c.shape)))
-            ops = [synth.uniform_torch(sd + 7 * j, c.shape, device=dev, start=rank * int(np.prod(c.shape)))
-                   for sd in c.operand_seeds]       # ADD operands (NEXT-1 residual stacks)
-            y = torch.empty(infos[c.name]["out"], device=dev)
+            chw = int(np.prod(c.shape[1:]))
+            x = synth.uniform_torch(c.input_seed + 7 * j + 1000 * s, c.shape, device=ctx.dev, start=lo * chw)
+            ops = [synth.uniform_torch(sd + 7 * j + 1000 * s, c.shape, device=ctx.dev, start=lo * chw)
+                   for sd in c.operand_seeds]
+            y = torch.empty(infos[c.name]["out"], device=ctx.dev)
             row.append(([x] + ops, y))
         bufs.append(row)
-    # dominant instance: the most algorithmic bytes
     dom = max(range(len(inst)), key=lambda j: infos[inst[j].name]["alg_bytes_read"] + infos[inst[j].name]["alg_bytes_written"])
-    dom_info = bs.bs_plan_query_launch(plans[inst[dom].name], 0)
     dom_bytes = infos[inst[dom].name]["alg_bytes_read"] + infos[inst[dom].name]["alg_bytes_written"]
-
-    stream = torch.cuda.Stream(device=dev)
-    sh = stream.cuda_stream
     handles = [plans[c.name] for c in inst]
 
-    def launch(h, xs, y, st_handle):
-        if len(xs) == 1:
-            bs.bs_execute(h, xs[0].data_ptr(), y.data_ptr(), st_handle)
-        else:
-            bs.bs_execute_ex(h, [t.data_ptr() for t in xs], y.data_ptr(), st_handle)
-
-    def step(k, st_handle):
+    def eager_step(k):
         row = bufs[k % n_sets]
         for j, h in enumerate(handles):
             xs, y = row[j]
-            launch(h, xs, y, st_handle)
+            ctx.launch(h, xs, y)
 
-    # eager warm-up (also JIT-loads every kernel), then one CUDA graph per buffer set so the
-    # timed region measures the device, not the Python launch loop
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(ctx.stream):
         for k in range(args.warmup):
-            step(k, sh)
+            eager_step(k)
     torch.cuda.synchronize()
     # one CUDA graph per buffer set over every stack of the step, built by the library's own
     # bs_graph API (NEXT-3): a step is a single host call
-    graphs = []
-    if not args.no_graph:
-        for sidx in range(n_sets):
-            graphs.append(bs.bs_graph_create([(h, bufs[sidx][j][0], bufs[sidx][j][1]) for j, h in enumerate(handles)]))
-        torch.cuda.synchronize()
+    graphs = [bs.bs_graph_create([(h, bufs[s][j][0], bufs[s][j][1]) for j, h in enumerate(handles)])
+              for s in range(n_sets)]
+    torch.cuda.synchronize()
 
     def run_step(k):
-        if graphs:
-            bs.bs_graph_launch(graphs[k % n_sets], sh)
-        else:
-            step(k, sh)
+        bs.bs_graph_launch(graphs[k % n_sets], ctx.sh)
 
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(ctx.stream):
         for k in range(args.warmup):
             run_step(k)
     torch.cuda.synchronize()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
+    t_start, t_end = ctx.event(), ctx.event()
+    ctx.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        with torch.cuda.stream(stream):
-            t_start.record(stream)
+    with ClockSampler(ctx.local) as clk:
+        w0 = time.perf_counter()
+        with torch.cuda.stream(ctx.stream):
+            t_start.record(ctx.stream)
             for k in range(args.steps):
                 run_step(args.warmup + k)
-            t_end.record(stream)
+            t_end.record(ctx.stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = t_start.elapsed_time(t_end)
+        wall = time.perf_counter() - w0
+    ctx.barrier()
+    ev_ms = t_start.elapsed_time(t_end)
+    agg = aggregate(batch, ev_ms, wall, args.steps, ctx.dev)
 
-    # per-step min / median (SURVEY §8(d) protocol), outside the timed region: 20 steps each
-    # bracketed by its own events (serialised, so each includes its own ramp and drain)
-    per_step = []
-    with torch.cuda.stream(stream):
-        for k in range(20):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            run_step(k)
-            e1.record(stream)
-            e1.synchronize()
-            per_step.append(e0.elapsed_time(e1))
-    step_min, step_med = float(np.min(per_step)), float(np.median(per_step))
+    res = {"workload": wl, "baseline_config_index": CONFIG_INDEX[wl], "scaling": "strong" if strong else "weak",
+           "global_batch": agg["images_per_step"], "per_gpu_batch": batch, "stacks_per_step": len(inst),
+           "launches_per_step": launches_per_step, "value": agg["images_per_s"], "ms_per_step": agg["ms_per_step"],
+           "timing": {k: agg[k] for k in ("event_ms_max", "wall_s_max", "timer")},
+           "clocks": clk.summary()}
+    gbs_rank = step_bytes / (ev_ms / args.steps / 1e3) / 1e9
+    res["hbm"] = {"alg_gbs_per_gpu": gbs_rank, "alg_gbs_total": step_bytes * ctx.world / (agg["ms_per_step"] / 1e3) / 1e9,
+                  "pct_of_measured_peak": 100 * gbs_rank / ctx.peak, "pct_of_8tbs": 100 * gbs_rank / 8000.0,
+                  "alg_bytes_per_step_per_gpu": step_bytes}
+    res["l2"] = (f"rotating {n_sets} buffer sets ({n_sets * step_bytes / 1e9:.2f} GB > 4x L2 {ctx.l2 / 1e6:.0f} MB)"
+                 if n_sets > 1 else f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB per step vs {ctx.l2 / 1e6:.0f} MB)")
 
-    # dominant kernel alone: D back-to-back launches over rotating buffer sets (one graph),
+    if full:   # per-step min / median (SURVEY §8(d) protocol), outside the timed region
+        per_step = []
+        with torch.cuda.stream(ctx.stream):
+            for k in range(20):
+                e0, e1 = ctx.event(), ctx.event()
+                e0.record(ctx.stream)
+                run_step(k)
+                e1.record(ctx.stream)
+                e1.synchronize()
+                per_step.append(e0.elapsed_time(e1))
+        res["ms_per_step_isolated"] = {"min": float(np.min(per_step)), "median": float(np.median(per_step)),
+                                       "n": len(per_step)}
+
+    # dominant kernel alone: D back-to-back launches over rotating buffer sets (one bs_graph),
     # CUDA events on the launching stream around the replays -> average launch duration
-    D = max(4, min(50, int(4 * l2 // max(1, dom_bytes)) + 4))
-    dom_sets = max(n_sets, int(math.ceil(4 * l2 / dom_bytes)) + 1)
-    dbufs = [bufs[sidx % n_sets][dom] if sidx < n_sets else
-             ([synth.uniform_torch(sd + 99 * sidx, inst[dom].shape, device=dev)
+    D = max(4, min(50, int(4 * ctx.l2 // max(1, dom_bytes)) + 4))
+    dom_sets = max(n_sets, int(math.ceil(4 * ctx.l2 / dom_bytes)) + 1)
+    dbufs = [bufs[s % n_sets][dom] if s < n_sets else
+             ([synth.uniform_torch(sd + 99 * s, inst[dom].shape, device=ctx.dev)
                for sd in [inst[dom].input_seed] + inst[dom].operand_seeds],
-              torch.empty(infos[inst[dom].name]["out"], device=dev)) for sidx in range(dom_sets)]
+              torch.empty(infos[inst[dom].name]["out"], device=ctx.dev)) for s in range(dom_sets)]
     dh = handles[dom]
-
-    def dom_burst(st_handle):
-        for r in range(D):
-            xs, y = dbufs[r % dom_sets]
-            launch(dh, xs, y, st_handle)
-
-    with torch.cuda.stream(stream):
-        dom_burst(sh)
-    torch.cuda.synchronize()
-    dg = None
-    if not args.no_graph:
-        dg = bs.bs_graph_create([(dh, dbufs[r % dom_sets][0], dbufs[r % dom_sets][1]) for r in range(D)])
-    da, db = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dg = bs.bs_graph_create([(dh, dbufs[r % dom_sets][0], dbufs[r % dom_sets][1]) for r in range(D)])
+    da, db = ctx.event(), ctx.event()
     reps = 5
-    with torch.cuda.stream(stream):
-        (bs.bs_graph_launch(dg, sh) if dg else dom_burst(sh))
-        da.record(stream)
+    with torch.cuda.stream(ctx.stream):
+        bs.bs_graph_launch(dg, ctx.sh)
+        da.record(ctx.stream)
         for _ in range(reps):
-            (bs.bs_graph_launch(dg, sh) if dg else dom_burst(sh))
-        db.record(stream)
+            bs.bs_graph_launch(dg, ctx.sh)
+        db.record(ctx.stream)
     torch.cuda.synchronize()
     dom_ms = da.elapsed_time(db) / (reps * D)
-    # checksum of the last step's outputs (fp64 sum) -- gathered below, outside the timing
+    del dg, dbufs
+    from paper_1804_08378_b200 import dist as bsd
+    dom_ms = bsd.max_over_ranks([dom_ms], ctx.dev)[0]
+    dom_li = bs.bs_plan_query_launch(plans[inst[dom].name], 0)
+    dom_achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    res["roofline"] = {"bound": "hbm", "achieved": dom_achieved, "peak": ctx.peak, "unit": "GB/s",
+                       "frac": dom_achieved / ctx.peak, "traffic": None, "peak_source": ctx.peak_src,
+                       "kernel": bs.KERNEL_NAMES[dom_li["kernel"]], "stack": inst[dom].name,
+                       "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
+                       "how": f"{D} back-to-back launches over {dom_sets} rotating buffer sets, CUDA events"}
+    res["roofline"].update(stored_traffic(wl, inst[dom].name, dom_bytes))
+
+    # checksums of the last timed step (fp64 sum per stack output) and validation of the
+    # dominant stack: all-gather its output shards, compare sampled global images with the oracle
     last = bufs[(args.warmup + args.steps - 1) % n_sets]
     csum = float(sum(y.double().sum().item() for _, y in last))
     finite = all(bool(torch.isfinite(y).all()) for _, y in last)
-    # max over ranks of the device times; per-rank checksums (outside the timed region)
-    ms, dom_ms = bsd.max_over_ranks([ms, dom_ms], dev)
-    gathered = bsd.gather_stats([csum, float(finite), float(batch)], dev)
-    checksums = [g[0] for g in gathered]
-    finite = all(bool(g[1]) for g in gathered)
-    images = int(sum(g[2] for g in gathered))
+    g = bsd.gather_stats([csum, float(finite)], ctx.dev)
+    res["checksums"] = [r[0] for r in g]
+    res["outputs_finite"] = all(bool(r[1]) for r in g)
+    if not args.no_validate:
+        res["validation"] = validate_dominant(ctx, inst[dom], last[dom], dom, n_total, lo,
+                                              (args.warmup + args.steps - 1) % n_sets)
+    res["_internal"] = {"cases": cases, "plans": plans, "infos": infos, "inst": inst, "bufs": bufs,
+                        "n_sets": n_sets, "batch": batch, "handles": handles}
+    return res
 
-    ms_step = ms / args.steps
-    ips = images / (ms_step / 1e3)
-    gbs_rank = step_bytes / (ms_step / 1e3) / 1e9
-    peak, peak_src = load_peaks()
-    dom_achieved = dom_bytes / (dom_ms / 1e3) / 1e9
 
-    # ---- optional per-stack breakdown (same burst method as the dominant kernel)
-    per_stack = None
-    if args.per_stack:
-        per_stack = []
-        peak_, _ = load_peaks()
-        for c in cases:
-            nb = infos[c.name]["alg_bytes_read"] + infos[c.name]["alg_bytes_written"]
-            nset = int(math.ceil(4 * l2 / nb)) + 1
-            sb = [([synth.uniform_torch(sd + 13 * q, c.shape, device=dev) for sd in [c.input_seed] + c.operand_seeds],
-                   torch.empty(infos[c.name]["out"], device=dev)) for q in range(min(nset, 64))]
-            R = max(8, min(64, len(sb) * 2))
-            hh = plans[c.name]
+def validate_dominant(ctx, case, buf, j, n_total, lo, set_idx):
+    """All-gather the dominant stack's output shards (outside the timed region) and compare
+    sampled global images with the CPU oracle on rank 0."""
+    from paper_1804_08378_b200 import dist as bsd
+    xs, y = buf
+    out = bsd.gather_shards(y, n_total, ctx.dev) if ctx.world > 1 else y
+    if ctx.rank != 0:
+        return None
+    import oracle
+    from tests import _util as U
+    oracle.build()
+    chw = int(np.prod(case.shape[1:]))
+    shp = (1,) + tuple(case.shape[1:])
+    base = case.input_seed + 7 * j + 1000 * set_idx
 
-            def burst(st_handle):
-                for r in range(R):
-                    xs, y = sb[r % len(sb)]
-                    launch(hh, xs, y, st_handle)
-            with torch.cuda.stream(stream):
-                burst(sh)
-            torch.cuda.synchronize()
-            gg = bs.bs_graph_create([(hh, sb[r % len(sb)][0], sb[r % len(sb)][1]) for r in range(R)])
-            with torch.cuda.stream(stream):
-                bs.bs_graph_launch(gg, sh)
-                da.record(stream)
-                for _ in range(3):
-                    bs.bs_graph_launch(gg, sh)
-                db.record(stream)
-            torch.cuda.synchronize()
-            t = da.elapsed_time(db) / (3 * R)
-            li = bs.bs_plan_query_launch(hh, 0)
-            per_stack.append({"stack": c.name, "count": c.count, "shape": list(c.shape), "ms": t,
-                              "gbs": nb / (t / 1e3) / 1e9, "frac": nb / (t / 1e3) / 1e9 / peak_,
-                              "kernel": bs.KERNEL_NAMES[li["kernel"]]})
-            del sb, gg
+    def ref_image(n):
+        x = synth.uniform_np(base, chw, start=n * chw).reshape(shp)
+        ops = [synth.uniform_np(sd + 7 * j + 1000 * set_idx, chw, start=n * chw).reshape(shp)
+               for sd in case.operand_seeds]
+        return oracle.run_bf(case.layers, x, ops)
 
-    # ---- end to end: host buffers through bs_execute_host (H2D + kernels + D2H every step)
-    e2e = None
+    gathered = out.cpu().numpy() if hasattr(out, "cpu") else out
+    r = validate_gathered(gathered, n_total, ref_image, lambda got, ref, ctx_: U.check(got, ref, case.layers, ctx_))
+    r["stack"] = case.name
+    r["gathered_images"] = int(gathered.shape[0])
+    return r
+
+
+def stored_traffic(wl, stack, alg_bytes):
+    """ncu DRAM bytes per launch of the dominant stack, from profiles/ncu_traffic.json -- used only
+    if it was captured from the current kernel sources (keyed by their hash), else null."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    out = {"traffic_source": None}
+    if not os.path.exists(p):
+        return out
+    tr = json.load(open(p))
+    e = tr.get("entries", {}).get(f"{wl}:{stack}")
+    if e is None:
+        return out
+    if tr.get("sources_sha16") != kernel_sources_hash():
+        out["traffic_source"] = f"stale: {p} was captured from kernel sources {tr.get('sources_sha16')}"
+        return out
+    out["traffic"] = e["dram_bytes_per_launch"]
+    out["traffic_ratio_to_alg"] = e["dram_bytes_per_launch"] / alg_bytes
+    out["traffic_source"] = f"ncu --set full, {tr.get('captured')} ({os.path.relpath(p, ROOT)})"
+    return out
+
+
+def measure_e2e(ctx, m):
+    """End to end through bs_execute_host: every step copies each stack's inputs from pinned host
+    memory, runs the kernels and copies the outputs back (pipelined per image chunk)."""
+    torch, bs, args = ctx.torch, ctx.bs, ctx.args
+    I = m["_internal"]
+    cases, infos, inst, bufs, n_sets, handles = I["cases"], I["infos"], I["inst"], I["bufs"], I["n_sets"], I["handles"]
     e2e_steps = args.e2e_steps or max(3, min(20, args.steps // 10))
     max_in = max(infos[c.name]["alg_bytes_read"] // (1 + len(c.operand_seeds)) for c in cases) // 4
     max_out = max(infos[c.name]["alg_bytes_written"] for c in cases) // 4
     h_in = torch.empty(max_in, dtype=torch.float32).pin_memory()
-    h_in.copy_(synth.uniform_torch(99, (max_in,), device=dev).cpu())
+    h_in.copy_(synth.uniform_torch(99, (max_in,), device=ctx.dev).cpu())
     h_out = torch.empty(max_out, dtype=torch.float32).pin_memory()
     h2d = sum(infos[c.name]["alg_bytes_read"] for c in inst)
     d2h = sum(infos[c.name]["alg_bytes_written"] for c in inst)
@@ -422,158 +580,213 @@ def main():
         row = bufs[k % n_sets]
         for j, h in enumerate(handles):
             xs, y = row[j]
-            # every input (stack input and ADD operands) is copied from pinned host memory
             bs.bs_execute_host(h, [h_in.data_ptr()] * len(xs), h_out.data_ptr(), [t.data_ptr() for t in xs],
-                               y.data_ptr(), 0, sh)
+                               y.data_ptr(), 0, ctx.sh)
 
     e2e_step(0)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
+    ctx.barrier()
+    a, b = ctx.event(), ctx.event()
+    w0 = time.perf_counter()
+    a.record(ctx.stream)
     for k in range(e2e_steps):
         e2e_step(k)
-    b.record(stream)
+    b.record(ctx.stream)
     torch.cuda.synchronize()
-    e2e_ms = a.elapsed_time(b)
-    e2e_ms = bsd.max_over_ranks([e2e_ms], dev)[0]
-    # the e2e roofline: host -> device bandwidth of a plain pinned copy of the same bytes
-    probe = int(min(h2d, 256 << 20))   # (at most 256 MB of pinned memory for the probe)
+    wall = time.perf_counter() - w0
+    ctx.barrier()
+    agg = aggregate(I["batch"], a.elapsed_time(b), wall, e2e_steps, ctx.dev)
+    # the e2e roofline: host <-> device bandwidth of a plain pinned copy of the same bytes
+    probe = int(min(h2d, 256 << 20))
     hb = torch.empty(probe // 4, dtype=torch.float32).pin_memory()
-    db = torch.empty(probe // 4, dtype=torch.float32, device=dev)
+    dbuf = torch.empty(probe // 4, dtype=torch.float32, device=ctx.dev)
     pcie_gbs = d2h_gbs = 0.0
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(ctx.stream):
         for r in range(7):   # 2 warm-up copies each way, then the best of 5
-            a.record(stream)
-            db.copy_(hb, non_blocking=True)
-            b.record(stream)
+            a.record(ctx.stream)
+            dbuf.copy_(hb, non_blocking=True)
+            b.record(ctx.stream)
             torch.cuda.synchronize()
             if r >= 2:
                 pcie_gbs = max(pcie_gbs, probe / (a.elapsed_time(b) / 1e3) / 1e9)
-            a.record(stream)
-            hb.copy_(db, non_blocking=True)
-            b.record(stream)
+            a.record(ctx.stream)
+            hb.copy_(dbuf, non_blocking=True)
+            b.record(ctx.stream)
             torch.cuda.synchronize()
             if r >= 2:
                 d2h_gbs = max(d2h_gbs, probe / (a.elapsed_time(b) / 1e3) / 1e9)
-    del hb, db
-    e2e_h2d_gbs = h2d / (e2e_ms / e2e_steps / 1e3) / 1e9
-    # the binding direction: the step cannot beat max(H2D time, D2H time) at the probed rates
+    del hb, dbuf
+    t_step = agg["ms_per_step"] / 1e3
     t_bound = max(h2d / (pcie_gbs * 1e9), d2h / (d2h_gbs * 1e9))
-    bound_frac = t_bound / (e2e_ms / e2e_steps / 1e3)
-    e2e = {"value": images / (e2e_ms / e2e_steps / 1e3), "unit": "images/s", "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
-           "path": "bs_execute_host: pinned host -> device copy, kernels, device -> host copy, pipelined per chunk",
-           "roofline": {"bound": "pcie_h2d" if h2d / pcie_gbs >= d2h / d2h_gbs else "pcie_d2h",
-                        "achieved_gbs": e2e_h2d_gbs, "peak_gbs": pcie_gbs, "d2h_peak_gbs": d2h_gbs,
-                        "frac": bound_frac,
-                        "peak_source": "measured: best of 5 pinned host <-> device torch copies (<= 256 MB each way); frac = max(H2D, D2H) time at those rates / step time"}}
+    return {"value": agg["images_per_s"], "unit": "images/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": e2e_steps, "timer": agg["timer"],
+            "path": "bs_execute_host: pinned host -> device copy, kernels, device -> host copy, pipelined per chunk",
+            "roofline": {"bound": "pcie_h2d" if h2d / pcie_gbs >= d2h / d2h_gbs else "pcie_d2h",
+                         "achieved_gbs": h2d / t_step / 1e9, "peak_gbs": pcie_gbs, "d2h_peak_gbs": d2h_gbs,
+                         "frac": t_bound / t_step,
+                         "peak_source": "measured: best of 5 pinned host <-> device torch copies (<= 256 MB each way); "
+                                        "frac = max(H2D, D2H) time at those rates / step time"}}
 
-    # ---- layer-by-layer torch eager on the same GPU (the paper's comparison system, re-hosted)
-    lbl = None
-    if not args.no_lbl and rank == 0:
-        import torch.nn.functional as F
-        params = {}
-        for c in cases:
-            ps = []
-            for L in c.layers:
+
+def measure_lbl(ctx, m):
+    """Layer-by-layer torch eager on the same GPU and tensors (the paper's comparison system)."""
+    import torch.nn.functional as F
+    torch, args = ctx.torch, ctx.args
+    I = m["_internal"]
+    cases, inst, bufs, n_sets = I["cases"], I["inst"], I["bufs"], I["n_sets"]
+    params = {}
+    for c in cases:
+        params[c.name] = [tuple(torch.from_numpy(getattr(L, f)).to(ctx.dev) for f in ("mean", "var", "gamma", "beta"))
+                          if L.kind == "batchnorm" else None for L in c.layers]
+
+    def lbl_step(k):
+        row = bufs[k % n_sets]
+        for j, c in enumerate(inst):
+            xs = row[j][0]
+            t = xs[0]
+            for L, p in zip(c.layers, params[c.name]):
                 if L.kind == "batchnorm":
-                    ps.append(tuple(torch.from_numpy(getattr(L, f)).to(dev) for f in ("mean", "var", "gamma", "beta")))
-                else:
-                    ps.append(None)
-            params[c.name] = ps
-
-        def lbl_step(k):
-            row = bufs[k % n_sets]
-            for j, c in enumerate(inst):
-                xs = row[j][0]
-                t = xs[0]
-                for L, p in zip(c.layers, params[c.name]):
-                    if L.kind == "batchnorm":
-                        t = F.batch_norm(t, p[0], p[1], p[2], p[3], False, 0.0, L.eps)
-                    elif L.kind == "relu":
-                        t = F.relu(t)
-                    elif L.kind == "maxpool":
-                        t = F.max_pool2d(t, L.kernel, L.stride, L.padding)
-                    elif L.kind == "avgpool":
-                        t = F.avg_pool2d(t, L.kernel, L.stride, L.padding, count_include_pad=L.count_include_pad)
-                    elif L.kind == "add":
-                        t = t + xs[L.operand]
-        lsteps = max(3, min(50, args.steps // 4))
-        with torch.cuda.stream(stream):
-            for k in range(3):
-                lbl_step(k)
-            torch.cuda.synchronize()
-            a.record(stream)
-            for k in range(lsteps):
-                lbl_step(k)
-            b.record(stream)
+                    t = F.batch_norm(t, p[0], p[1], p[2], p[3], False, 0.0, L.eps)
+                elif L.kind == "relu":
+                    t = F.relu(t)
+                elif L.kind == "maxpool":
+                    t = F.max_pool2d(t, L.kernel, L.stride, L.padding)
+                elif L.kind == "avgpool":
+                    t = F.avg_pool2d(t, L.kernel, L.stride, L.padding, count_include_pad=L.count_include_pad)
+                elif L.kind == "add":
+                    t = t + xs[L.operand]
+    lsteps = max(3, min(50, args.steps // 4))
+    a, b = ctx.event(), ctx.event()
+    with torch.cuda.stream(ctx.stream):
+        for k in range(3):
+            lbl_step(k)
         torch.cuda.synchronize()
-        lbl_ms = a.elapsed_time(b) / lsteps
-        lbl = {"images_per_s": batch / (lbl_ms / 1e3), "ms_per_step": lbl_ms,
-               "fused_speedup": lbl_ms / ms_step,
-               "what": "torch eager F.batch_norm/relu/max_pool2d/avg_pool2d, one kernel per layer, same GPU"}
+        a.record(ctx.stream)
+        for k in range(lsteps):
+            lbl_step(k)
+        b.record(ctx.stream)
+    torch.cuda.synchronize()
+    lbl_ms = a.elapsed_time(b) / lsteps
+    return {"images_per_s": I["batch"] / (lbl_ms / 1e3), "ms_per_step": lbl_ms,
+            "fused_speedup": lbl_ms / m["ms_per_step"],
+            "what": "torch eager F.batch_norm/relu/max_pool2d/avg_pool2d, one kernel per layer, same GPU"}
 
-    # ---- CPU oracle baseline on a bounded sample (rank 0, N=1 only)
+
+def per_stack(ctx, m):
+    I = m["_internal"]
+    return [measure_stack_alone(ctx, c, I["plans"][c.name], I["infos"][c.name]) for c in I["cases"]]
+
+
+def measure_c1(ctx):
+    """configs[0]: the single C1 stack on the GPU (one launch, latency-bound) and the CPU oracle in ms."""
+    torch, bs = ctx.torch, ctx.bs
+    case = synth.workload("c1")[0]
+    plan = bs.bs_plan_create(case.layers, case.shape)
+    info = bs.bs_plan_query(plan)
+    sb, R = stack_burst(ctx, case, plan, info["alg_bytes_read"] + info["alg_bytes_written"], 13)
+
+    def burst():
+        for r in range(R):
+            xs, y = sb[r % len(sb)]
+            ctx.launch(plan, xs, y)
+    gpu_ms = ctx.burst_ms(burst) / R
+    out = {"stack": "BN->ReLU->MaxPool2x2/s2 (1,16,32,32)", "gpu_ms_per_launch": gpu_ms,
+           "gpu_launch_how": f"{R} back-to-back launches in one CUDA graph, CUDA events"}
+    if ctx.rank == 0 and not ctx.args.no_cpu_baseline:
+        out["c1_oracle_ms"] = c1_oracle_ms()
+        out["c1_oracle_how"] = "oracle_run_bf (plain C, 1 thread, -O2 -ffp-contract=off), min of 5 runs (P:L656-658)"
+    return out
+
+
+def strip(m):
+    return {k: v for k, v in m.items() if not k.startswith("_")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="brainslug", choices=["brainslug", "reference"])
+    ap.add_argument("--workload", default="resnet50", choices=list(CONFIG_INDEX))
+    ap.add_argument("--batch", type=int, default=0, help="per-rank (weak) / global (strong) batch; 0 = BASELINE.json's")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lbl", action="store_true", help="skip the torch layer-by-layer context number")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE workloads")
+    ap.add_argument("--no-per-stack", action="store_true", help="skip per-stack / ceiling timings")
+    ap.add_argument("--no-validate", action="store_true", help="skip the gathered-shard oracle check")
+    ap.add_argument("--out", default="", help="also append the JSON line to this file")
+    scal = ap.add_mutually_exclusive_group()
+    scal.add_argument("--strong", action="store_true", help="split every workload's BASELINE batch over ranks")
+    scal.add_argument("--weak", action="store_true", help="every rank runs its BASELINE batch (also DenseNet-121)")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+    import benchlib
+    benchlib.build()
+
+    ctx = Ctx(args)
+    do_stacks = not args.no_per_stack and ctx.world == 1
+    m = measure(ctx, args.workload, full=True)
+    e2e = measure_e2e(ctx, m)
+    lbl = measure_lbl(ctx, m) if (not args.no_lbl and ctx.rank == 0) else None
+    stacks = per_stack(ctx, m) if do_stacks else None
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, n, T = time_oracle(cases, args.cpu_budget, 1 << 20)
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
+        v, n, T = time_oracle(m["_internal"]["cases"], args.cpu_budget, 1 << 20)
         cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle", "host_cores": os.cpu_count(),
                "host_cpu": _cpu_model(),
-               "sample": f"{n} synthetic images shaped like the batch-{batch} {args.workload} workload (all stacks), "
-                         f"breadth-first C oracle, single thread, {T:.1f} s"}
+               "sample": f"{n} synthetic images shaped like the batch-{m['per_gpu_batch']} {args.workload} workload "
+                         f"(all stacks), breadth-first C oracle, single thread, {T:.1f} s"}
+    del m["_internal"]
+    extras = {}
+    if not args.no_extra:
+        for wl in EXTRA_WORKLOADS:
+            if wl == args.workload:
+                continue
+            mw = measure(ctx, wl, full=False)
+            if do_stacks:
+                mw["per_stack"] = per_stack(ctx, mw)
+            del mw["_internal"]
+            extras[wl] = mw
+        extras["c1"] = measure_c1(ctx)
 
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        tr = json.load(open(tp))
-        key = f"{args.workload}:{inst[dom].name}"
-        if key in tr:
-            traffic = tr[key]["dram_bytes_per_launch"]
-
-    if rank == 0:
+    if ctx.rank == 0:
         line = {
-            "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_isolated": {"min": step_min, "median": step_med, "n": len(per_step)},
-            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (SplitMix64 seeded NCHW fp32, BN params per SURVEY §8(d))",
+            "metric": METRIC, "value": m["value"], "unit": "images/s", "n_gpus": ctx.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": m["ms_per_step"],
+            "ms_per_step_isolated": m.get("ms_per_step_isolated"),
+            "higher_is_better": True, "scaling": m["scaling"], "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (SplitMix64 seeded NCHW fp32, BN params per SURVEY §8(d))",
             "config": {"workload": args.workload, "baseline_config_index": CONFIG_INDEX[args.workload],
-                       "global_batch": images, "per_gpu_batch": batch, "stacks_per_step": len(inst),
-                       "backend": backend if world > 1 else None,
-                       "parallelism": f"batch-sharded dp{world} (independent images, no data-path collective)",
-                       "launch": "one bs_graph (CUDA graph of every stack) replay per step" if graphs else "eager launches",
-                       "l2": (f"rotating {n_sets} buffer sets ({n_sets * step_bytes / 1e9:.2f} GB > 4x L2 "
-                              f"{l2 / 1e6:.0f} MB)") if n_sets > 1 else
-                             f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB per step vs {l2 / 1e6:.0f} MB)"},
-            "hbm": {"alg_gbs_per_gpu": gbs_rank, "alg_gbs_total": gbs_rank * world,
-                    "pct_of_measured_peak": 100 * gbs_rank / peak, "pct_of_8tbs": 100 * gbs_rank / 8000.0,
-                    "alg_bytes_per_step_per_gpu": step_bytes},
-            "roofline": {"bound": "hbm", "achieved": dom_achieved, "peak": peak, "unit": "GB/s",
-                         "frac": dom_achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": bs.KERNEL_NAMES[dom_info["kernel"]], "stack": inst[dom].name,
-                         "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
-                         "how": f"{D} back-to-back launches over {dom_sets} rotating buffer sets, CUDA events"},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk.summary(),
-            "layer_by_layer_torch": lbl,
-            "checksums": checksums, "outputs_finite": finite,
+                       "global_batch": m["global_batch"], "per_gpu_batch": m["per_gpu_batch"],
+                       "stacks_per_step": m["stacks_per_step"],
+                       "backend": ctx.backend if ctx.world > 1 else None,
+                       "parallelism": f"batch-sharded dp{ctx.world} (independent images, no data-path collective)",
+                       "launch": "one bs_graph (CUDA graph of every stack) replay per step",
+                       "l2": m["l2"]},
+            "timing": m["timing"], "hbm": m["hbm"], "roofline": m["roofline"], "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": m["launches_per_step"] * args.steps,
+            "clocks": m["clocks"], "layer_by_layer_torch": lbl,
+            "checksums": m["checksums"], "outputs_finite": m["outputs_finite"], "validation": m.get("validation"),
             # the paper's own numbers, quoted with their hardware (context, not targets; BASELINE.md)
             "paper_context": {"best_whole_network_speedup_gpu": "35.7 % (GTX 1080 Ti, PyTorch 0.3.0 + cuDNN, fp32)",
                               "best_whole_network_speedup_cpu": "41.1 % (Xeon E5-2690v4, ISPC + TBB)",
                               "synthetic_blocks_gpu": "1.4-2.2x vs PyTorch (GTX 1080 Ti)",
                               "source": "PAPER.md P:L27-29, P:L689, P:L953"},
-            "per_stack": per_stack,
+            "per_stack": stacks,
+            "workloads": extras,
         }
         s = json.dumps(line)
         print(s, flush=True)
         if args.out:
             with open(args.out, "a") as f:
                 f.write(s + "\n")
-    if world > 1:
-        dist.destroy_process_group()
+    if ctx.world > 1:
+        ctx.dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -41,8 +41,13 @@ cudaError_t smem_kernel_setup(const void* fn) {
   std::lock_guard<std::mutex> lock(mu);
   if (done.count({fn, dev})) return cudaSuccess;
   int optin = 0;
+  cudaFuncAttributes fa;
   if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess) return e;
+  if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return e;
+  // static + dynamic shared memory must fit the opt-in limit
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - (int)fa.sharedSizeBytes)) != cudaSuccess)
+    return e;
 #ifndef BS_NO_CARVEOUT
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 (int)cudaSharedmemCarveoutMaxShared)) != cudaSuccess)

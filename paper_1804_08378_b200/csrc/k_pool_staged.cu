@@ -36,6 +36,17 @@ size_t pool_staged_smem(int tile_planes, int HW, int HWo, int stages) {
 }
 
 
+// Every consumer THREAD arrives on a stage's empty barrier once it has read the tile (256
+// arrivals per tile).  One arrive per warp after __syncwarp() is equally ordered under the PTX
+// memory model (release by lane 0 after the warp barrier), but compute-sanitizer racecheck does
+// not follow that chain and reports the next bulk copy into the stage as a race; per-thread
+// arrivals make the ordering explicit at <= 2 % cost (AlexNet stacks, profiles/r02_racecheck.md).
+#ifndef BS_WARP_ARRIVE
+constexpr int kEmptyArrivals = 32 * kStagedConsumerWarps;
+#else
+constexpr int kEmptyArrivals = kStagedConsumerWarps;
+#endif
+
 template <int KH, int KW, int SH, int SW, bool IS_MAX, bool PAD, int PC, int OC>
 __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -65,7 +76,7 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 2);                        // cp.async arrive (edges) + expect_tx (body)
-      mbar_init(&empty[s], kStagedConsumerWarps);    // every consumer warp, once per tile
+      mbar_init(&empty[s], kEmptyArrivals);          // every consumer warp (thread), once per tile
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -79,7 +90,12 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
       int s = 0;
       uint32_t ph = 0;
       for (int k = 0; k < my_tiles; ++k) {
-        if (k >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
+        if (k >= S) {
+          mbar_wait_sleep(&empty[s], ph ^ 1);
+#ifdef BS_PROXY_FENCE
+          fence_proxy_async_smem();
+#endif
+        }
         const int64_t p0 = BS_TILE_P0(k);
         const int np = (int)min((int64_t)P, pe - p0);
         const float* src = a.in + (a.plane0 + p0) * (int64_t)HW;
@@ -248,8 +264,12 @@ __global__ void __launch_bounds__(kStagedThreads) pool_staged(PoolArgs a) {
         }
       }
     }
+#ifndef BS_WARP_ARRIVE
+    mbar_arrive(&empty[s]);                  // input stage consumed (by this thread)
+#else
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);   // input stage consumed
+#endif
     if (++s == S) { s = 0; ph ^= 1; }
   }
 }

@@ -127,6 +127,12 @@ __device__ __forceinline__ void seq_fast_step(const SeqFastStep& f, uint32_t in_
   }
 }
 
+#ifdef BS_ARRIVE_ALL
+#define BS_SEQ_EMPTY_ARRIVER true
+#else
+#define BS_SEQ_EMPTY_ARRIVER (cw == 0 && lane == 0)
+#endif
+
 __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = (uint64_t*)smem;
@@ -142,7 +148,11 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 2);
+#ifdef BS_ARRIVE_ALL
+      mbar_init(&empty[s], 32 * kSeqWarps);
+#else
       mbar_init(&empty[s], 1);
+#endif
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -155,7 +165,12 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
       int k = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
         const int s = k % a.stages;
-        if (k >= a.stages) mbar_wait_sleep(&empty[s], ((k / a.stages) - 1) & 1);
+        if (k >= a.stages) {
+          mbar_wait_sleep(&empty[s], ((k / a.stages) - 1) & 1);
+#ifdef BS_PROXY_FENCE
+          fence_proxy_async_smem();
+#endif
+        }
         const int64_t pl0 = (int64_t)t * a.tile_planes;
         const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
         const float* src = a.in + (a.plane0 + pl0) * (int64_t)HW0;
@@ -224,7 +239,7 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
           else seq_fast_step<false, false>(f, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
         }
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kSeqWarps) : "memory");   // step boundary
-        if (st_i == 0 && cw == 0 && lane == 0) mbar_arrive(&empty[s]);   // stage buffer consumed
+        if (st_i == 0 && BS_SEQ_EMPTY_ARRIVER) mbar_arrive(&empty[s]);   // stage buffer consumed
         continue;
       }
       // work items: (plane, output row, 32-column chunk); lane = output column
@@ -247,7 +262,7 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
         else out_buf[p * HWo + i * st.Wo + j] = r;
       }
       asm volatile("bar.sync 1, %0;" ::"r"(32 * kSeqWarps) : "memory");   // step boundary
-      if (st_i == 0 && cw == 0 && lane == 0) mbar_arrive(&empty[s]);   // stage buffer consumed
+      if (st_i == 0 && BS_SEQ_EMPTY_ARRIVER) mbar_arrive(&empty[s]);   // stage buffer consumed
     }
   }
 }

@@ -225,7 +225,7 @@ def test_broadcast_add_operand_checked_at_run_time(cuda_dev):
     assert torch.equal(got, ref)
     st = fe.BrainSlugStack([fe.LayerSpec("relu"), fe.LayerSpec("add", operand=1)], "bad")
     with pytest.raises(RuntimeError, match="does not broadcast"):
-        st(x, torch.zeros(3, 1, 1, device="cuda"))
+        st(x, torch.zeros(4, 1, 1, device="cuda"))
     with torch.no_grad():   # shape arithmetic stays an int through a classified stack
         gm2 = fe.optimize(_ShapeArith().eval())
         assert torch.equal(gm2(x), _ShapeArith()(x))

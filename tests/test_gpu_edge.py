@@ -56,7 +56,7 @@ WIDE = [
     ((1, 1, 8, 1030), lambda C: [synth.maxpool(3, 1, 1)]),                             # n_cc = 33
     ((1, 1, 4, 1031), lambda C: [synth.maxpool(2, 2)]),
     ((2, 3, 9, 1111), lambda C: [synth.batchnorm(C, 7), synth.relu(), synth.avgpool(3, 2, 1)]),
-    ((1, 2, 14, 3585), lambda C: [synth.relu(), synth.avgpool(7, 7)]),
+    ((1, 2, 7, 3591), lambda C: [synth.relu(), synth.avgpool(7, 7)]),                 # Wo = 513
 ]
 
 
@@ -77,9 +77,10 @@ def test_wide_planes(case, cuda_dev, oracle_lib):
 
 
 def test_staged_many_items_forced(cuda_dev, oracle_lib):
-    """AlexNet-shaped planes with one output column per lane group: 27+ column chunks per tile."""
+    """Narrow forced column groups (1-3 output columns per lane group, G = 32/J planes per warp):
+    5-13 column chunks x up to 13 row bands, far more than 16 items per tile."""
     bs = _bs()
-    shape = (2, 6, 55, 55)
+    shape = (4, 16, 27, 27)
     layers = [synth.relu(), synth.maxpool(3, 2)]
     x = synth.uniform_np(77, int(np.prod(shape))).reshape(shape)
     ref = oracle.run_bf(layers, x)
