@@ -143,10 +143,11 @@ def shard_of(n_total: int, world: int, rank: int, strong: bool):
 
 
 def aggregate(images_local: int, event_ms_local: float, wall_s_local: float, steps: int, device="cpu"):
-    """Whole-job rate of a timed region bracketed by barriers on every rank.  The job time is the
-    slower of the max-over-ranks device time and the max-over-ranks host wall-clock between the
-    barriers: ranks whose work does not really overlap (several ranks on one GPU) cannot add up
-    to more than the device delivers."""
+    """Whole-job rate of a timed region bracketed by barriers on every rank.  wall_s_local runs from
+    the release of the opening barrier to the release of the closing one (so it spans every rank's
+    work); the job time is the slower of the max-over-ranks device time and the max-over-ranks wall
+    time: ranks whose work does not really overlap (several ranks on one GPU) cannot add up to
+    more than the device delivers."""
     from paper_1804_08378_b200 import dist as bsd
     g = bsd.gather_stats([float(images_local), float(event_ms_local), float(wall_s_local)], device)
     images = int(round(sum(r[0] for r in g)))
@@ -425,9 +426,12 @@ def measure(ctx, wl: str, full: bool):
             run_step(k)
     torch.cuda.synchronize()
     t_start, t_end = ctx.event(), ctx.event()
-    ctx.barrier()
+    clk = ClockSampler(ctx.local)      # NVML init before the barrier: it takes tens of ms
     torch.cuda.synchronize()
-    with ClockSampler(ctx.local) as clk:
+    with clk:
+        # wall-clock from the release of the opening barrier to the release of the closing one:
+        # the job time of all ranks together
+        ctx.barrier()
         w0 = time.perf_counter()
         with torch.cuda.stream(ctx.stream):
             t_start.record(ctx.stream)
@@ -435,8 +439,8 @@ def measure(ctx, wl: str, full: bool):
                 run_step(args.warmup + k)
             t_end.record(ctx.stream)
         torch.cuda.synchronize()
+        ctx.barrier()
         wall = time.perf_counter() - w0
-    ctx.barrier()
     ev_ms = t_start.elapsed_time(t_end)
     agg = aggregate(batch, ev_ms, wall, args.steps, ctx.dev)
 
@@ -585,16 +589,16 @@ def measure_e2e(ctx, m):
 
     e2e_step(0)
     torch.cuda.synchronize()
-    ctx.barrier()
     a, b = ctx.event(), ctx.event()
+    ctx.barrier()
     w0 = time.perf_counter()
     a.record(ctx.stream)
     for k in range(e2e_steps):
         e2e_step(k)
     b.record(ctx.stream)
     torch.cuda.synchronize()
-    wall = time.perf_counter() - w0
     ctx.barrier()
+    wall = time.perf_counter() - w0
     agg = aggregate(I["batch"], a.elapsed_time(b), wall, e2e_steps, ctx.dev)
     # the e2e roofline: host <-> device bandwidth of a plain pinned copy of the same bytes
     probe = int(min(h2d, 256 << 20))

@@ -47,8 +47,8 @@ def main():
             else:
                 time.sleep(t_step)                # a device of its own
                 dev_s += t_step
-        wall = time.perf_counter() - w0
         dist.barrier()
+        wall = time.perf_counter() - w0
         agg = bench.aggregate(8, 1e3 * dev_s, wall, steps, "cpu")
         res["shared" if shared else "own"] = agg
     # ---- validation of gathered shards (strong and weak layouts)
