@@ -164,6 +164,8 @@ def validate_gathered(gathered, n_total: int, ref_image, check, samples=3):
     """Compare sampled global images of an all-gathered output with a reference (the oracle).
     ref_image(n) -> expected output of image n (1, C, Ho, Wo); check(got, ref, ctx) raises."""
     idx = sorted({0, n_total // 2, n_total - 1} | {int(v) for v in np.linspace(0, n_total - 1, samples)})
+    if os.environ.get("BS_VALIDATE_ALL"):
+        idx = list(range(n_total))
     errs = []
     for n in idx:
         try:
@@ -398,6 +400,7 @@ def measure(ctx, wl: str, full: bool):
             y = torch.empty(infos[c.name]["out"], device=ctx.dev)
             row.append(([x] + ops, y))
         bufs.append(row)
+    torch.cuda.synchronize()           # inputs are generated on the default stream
     dom = max(range(len(inst)), key=lambda j: infos[inst[j].name]["alg_bytes_read"] + infos[inst[j].name]["alg_bytes_written"])
     dom_bytes = infos[inst[dom].name]["alg_bytes_read"] + infos[inst[dom].name]["alg_bytes_written"]
     handles = [plans[c.name] for c in inst]
@@ -479,6 +482,7 @@ def measure(ctx, wl: str, full: bool):
               torch.empty(infos[inst[dom].name]["out"], device=ctx.dev)) for s in range(dom_sets)]
     dh = handles[dom]
     dg = bs.bs_graph_create([(dh, dbufs[r % dom_sets][0], dbufs[r % dom_sets][1]) for r in range(D)])
+    torch.cuda.synchronize()           # the extra input sets are generated on the default stream
     da, db = ctx.event(), ctx.event()
     reps = 5
     with torch.cuda.stream(ctx.stream):
