@@ -94,9 +94,15 @@ typedef struct {
     int32_t device;                 /* CUDA device ordinal; -1 = current device */
     int32_t host_only;              /* 1 = plan on the host only (no device memory; the plan can
                                        be queried but not executed); used by CPU tests */
-    int32_t max_steps_per_sequence; /* 0 = unlimited (up to 16 steps and what fits on chip);
-                                       1 and 5 mirror the paper's policies.  A
-                                       sequence of >= 2 steps runs on-chip in one launch */
+    int32_t max_steps_per_sequence; /* steps per on-chip sequence (one launch):
+                                       0 = planner: as many as fit the shared-memory budget, and
+                                           for halo (row-band) tiles only while the band covers
+                                           its own input halo (bounded redundant work);
+                                       -1 = the paper's "unrestricted" strategy: as many as fit
+                                           (redundant halo work grows until a new sequence starts,
+                                           P:L718-729);
+                                       k >= 1: at most k (1 and 5 mirror P:L677-678).
+                                       Never more than 64 (the device step table) */
     int32_t threads_per_block;      /* must be 0: every kernel has a fixed block size tuned for
                                        sm_100a (256 or 32 x 9); other values -> INVALID_ARGUMENT */
     int32_t force_rows_per_task;    /* 0 = planner; >0 forces the output-row band of a pool
@@ -149,7 +155,9 @@ typedef struct {
     int32_t groups_per_warp;        /* lane groups (one plane each) packed in a warp */
     int32_t outputs_per_group;      /* output columns produced by one lane group */
     int32_t rows_per_task;          /* output rows walked by one warp task */
-    int32_t halo_rows;              /* input rows re-read between row bands (k - s, >= 0) */
+    int32_t halo_rows;              /* kernels 2-6: input rows re-read between row bands (k - s,
+                                       >= 0); kernel 7: step-0 input rows loaded in total over a
+                                       plane's bands beyond the plane's own rows (redundant halo) */
     int64_t n_tasks;                /* warp tasks (kernels 2-5), staged tiles (6, 7) */
     int64_t alg_bytes_read, alg_bytes_written;
     int32_t smem_bytes;             /* dynamic shared memory per CTA (0 for kernels 1-5) */

@@ -94,7 +94,13 @@ struct Launch {
   bool deferred = false;            // max pool: monotone prologue moved after the pool
   std::vector<Step> seq;            // K_SEQ: the steps of the on-chip sequence
   size_t seq_off = 0;               // K_SEQ: index of its first descriptor in the plan's array
+  size_t range_off = 0;             // K_SEQ: index of its first SeqRange in the plan's array
   int32_t seq_work_floats = 0;      // K_SEQ: floats per shared-memory work buffer
+  int32_t seq_bands = 1;            // K_SEQ: row bands per plane (1 = whole-plane tiles)
+  int32_t seq_band_rows = 0;        // K_SEQ: output rows of the last step per band
+  int32_t seq_stage_bytes = 0;      // K_SEQ: bytes per ring stage
+  std::vector<int32_t> seq_in_pitch, seq_out_pitch;   // K_SEQ: floats per plane, per step
+  std::vector<SeqRange> seq_ranges; // K_SEQ: [bands][steps]
   std::vector<HostOp> dev_pro, dev_epi;  // programs as the kernel runs them
   bs_launch_info info{};
 };
@@ -111,6 +117,7 @@ struct bs_plan {
   std::vector<Step> steps;             // every step of the stack, in order
   float2* params = nullptr;            // device parameter block
   SeqStepDev* seq_steps = nullptr;     // device descriptors of on-chip sequences
+  SeqRange* seq_ranges = nullptr;      // device per-band row ranges of on-chip sequences
   float* inter[2] = {nullptr, nullptr};  // intermediates between serialised sequences
   cudaStream_t copy_stream[2] = {nullptr, nullptr};  // bs_execute_host pipelines
   cudaEvent_t ev_pool[64] = {};
@@ -465,23 +472,203 @@ bool has_add(const Step& s) {
   return false;
 }
 
-// Shared memory of an on-chip sequence over steps [a, b) at P planes per tile, 2 stages.
-int64_t seq_bytes(const std::vector<Step>& st, size_t a, size_t b, int64_t P, int stages, int64_t* work_floats) {
-  const int64_t HW0 = st[a].in.h * st[a].in.w;
-  int64_t inter = 1;
-  for (size_t k = a; k + 1 < b; ++k) inter = std::max<int64_t>(inter, st[k].out.h * st[k].out.w);
-  if (work_floats) *work_floats = P * inter;
-  return 128 + stages * (int64_t)pool_staged_stride((int)P, (int)HW0) + 2 * P * inter * 4 + 256;
+// ---------------------------------------------------------------- a4: on-chip sequences
+// Geometry of an on-chip sequence over steps [a, b) (NEXT-2; k_seq.cu): P planes per tile and
+// bands of R output rows of the last step (R = Ho: whole planes).  For every band the rows of
+// every step are back-propagated through the windows (in_lo = out_lo*s - p,
+// in_hi = (out_hi-1)*s + k - p, clipped to the plane): a step computes the rows the next step
+// needs, so a band's input grows by the window overlap of every step -- the paper's redundant
+// halo work.  Shared memory = ring stages of step 0's input rows + two work buffers
+// of the largest intermediate band (the paper's "two buffers").
+struct SeqGeom {
+  int64_t P = 1, R = 0, n_bands = 1, stages = 2;
+  int64_t stage_bytes = 0, work_floats = 0, smem = 0;
+  std::vector<int32_t> in_pitch, out_pitch;
+  std::vector<SeqRange> ranges;
+};
+
+bool is_fast_step(const Step& st) {
+  return st.has_pool && st.is_max && st.kh == 3 && st.kw == 3 && st.sh == 1 && st.sw == 1 && st.ph == 1 &&
+         st.pw == 1 && st.pro.empty() && prog_class(st.epi) != PC_GENERIC && st.in.w % 4 == 0 && st.in.w <= 256;
 }
 
-// a4 sequence packing (lst:collapse #4): greedily add the next step while the
-// sequence still fits on chip -- here: whole planes of the first input and of every
-// intermediate in shared memory (no halos) -- and the policy's step limit allows it.
+// Rows of every step of [a, b) for the last step's output rows [o_lo, o_hi).
+void band_rows(const std::vector<Step>& st, size_t a, size_t b, int64_t o_lo, int64_t o_hi, SeqRange* out) {
+  for (size_t k = b; k-- > a;) {
+    const Step& s = st[k];
+    SeqRange& r = out[k - a];
+    std::memset(&r, 0, sizeof r);
+    r.out_lo = (int32_t)o_lo;
+    r.out_hi = (int32_t)o_hi;
+    int64_t lo = o_lo, hi = o_hi;
+    if (s.has_pool) {
+      lo = std::max<int64_t>(0, o_lo * s.sh - s.ph);
+      hi = std::min<int64_t>(s.in.h, (o_hi - 1) * s.sh - s.ph + s.kh);
+    }
+    r.in_lo = (int32_t)lo;
+    r.in_hi = (int32_t)hi;
+    o_lo = lo;
+    o_hi = hi;
+  }
+}
+
+// Fill g for P planes per tile, R output rows per band, S stages; returns the dynamic smem bytes.
+int64_t seq_geometry(const std::vector<Step>& st, size_t a, size_t b, int64_t P, int64_t R, int64_t S, SeqGeom& g) {
+  const size_t n = b - a;
+  const Step& last = st[b - 1];
+  const int64_t Ho = last.out.h;
+  R = std::max<int64_t>(1, std::min(R, Ho));
+  g.P = P;
+  g.R = R;
+  g.stages = S;
+  g.n_bands = (Ho + R - 1) / R;
+  g.ranges.assign((size_t)g.n_bands * n, SeqRange());
+  for (int64_t bd = 0; bd < g.n_bands; ++bd)
+    band_rows(st, a, b, bd * R, std::min(Ho, (bd + 1) * R), &g.ranges[(size_t)bd * n]);
+  std::vector<int64_t> rows_in(n, 0), rows_out(n, 0);
+  for (const SeqRange& r : g.ranges) {
+    const size_t k = (size_t)(&r - g.ranges.data()) % n;
+    rows_in[k] = std::max<int64_t>(rows_in[k], r.in_hi - r.in_lo);
+    rows_out[k] = std::max<int64_t>(rows_out[k], r.out_hi - r.out_lo);
+  }
+  const int64_t W0 = st[a].in.w;
+  g.stage_bytes = (P * rows_in[0] * W0 * 4 + 16 + 127) / 128 * 128;
+  g.in_pitch.assign(n, 0);
+  g.out_pitch.assign(n, 0);
+  g.in_pitch[0] = (int32_t)(g.n_bands == 1 ? st[a].in.h * W0 : rows_in[0] * W0);
+  int64_t wf = 0;
+  for (size_t k = 0; k + 1 < n; ++k) {
+    const int64_t pitch = (rows_out[k] * st[a + k].out.w + 3) / 4 * 4;
+    g.out_pitch[k] = (int32_t)pitch;
+    g.in_pitch[k + 1] = (int32_t)pitch;
+    wf = std::max(wf, P * pitch);
+  }
+  g.work_floats = wf;
+  g.smem = 128 + S * g.stage_bytes + 2 * wf * 4 + 1024;
+  return g.smem;
+}
+
+// Fast-path chunking of each (band, step): enough (plane, row chunk, column segment) items for
+// the 8 consumer warps, chunks of >= 4 rows (each chunk re-reads two halo rows of its input).
+void seq_chunking(const std::vector<Step>& st, size_t a, size_t b, SeqGeom& g) {
+  const size_t n = b - a;
+  for (size_t idx = 0; idx < g.ranges.size(); ++idx) {
+    SeqRange& r = g.ranges[idx];
+    const Step& s = st[a + idx % n];
+    const int64_t nrows = std::max<int64_t>(1, r.out_hi - r.out_lo);
+    int64_t nch = 1;
+    if (is_fast_step(s)) {
+      const int64_t seg = s.in.w <= 64 ? 16 : 32, nseg = (s.in.w + 4 * seg - 1) / (4 * seg);
+      const int64_t want_half = (int64_t)kSeqWarps * (32 / seg);
+      nch = std::max<int64_t>(1, std::min<int64_t>((want_half + g.P * nseg - 1) / (g.P * nseg), nrows / 4));
+    }
+    const int64_t L = (nrows + nch - 1) / nch;
+    nch = (nrows + L - 1) / L;
+    r.n_chunks = (int32_t)nch;
+    r.L = (int32_t)L;
+    r.chunks = make_fastdiv((uint32_t)nch);
+  }
+}
+
+// Dynamic shared memory a sequence may use per CTA: whole-plane tiles may take the plan's cap
+// (one CTA per SM); halo tiles are planned against the paper's cache budget -- by default half
+// the SM (two CTAs per SM), or bs_plan_options.smem_budget_bytes.
+int64_t seq_band_cap(const bs_plan_options& o) {
+  return o.smem_budget_bytes > 0 ? smem_cap(o) : std::min<int64_t>(110 * 1024, smem_cap(o));
+}
+// Base halo tile (the paper's "one output value per SIMD unit"): the fewest rows of the
+// last step's output that give each of the 256 consumer lanes an output.
+int64_t seq_base_rows(const Step& last) { return std::max<int64_t>(1, (256 + last.out.w - 1) / last.out.w); }
+
+// a4 sequence packing: greedily add the next step while the sequence's
+// tile still fits the shared-memory budget -- whole planes, else a halo band of the base tile
+// size whose input grows with every added padded step -- and the policy's step limit allows it.
 // A step with an ADD operand (per-execute pointers) is kept in a sequence of its own.
-bool seq_fits(const std::vector<Step>& st, size_t a, size_t b, int64_t cap) {
+// The planner's default policy (max_steps_per_sequence = 0) bounds the halo redundancy on top of
+// that: a halo-tiled sequence takes another step only while the largest band that fits still
+// covers at least as many output rows as its step-0 input halo (halo rows <= band rows, i.e. at
+// most 2x the input rows and ~1.5x the step work).  The paper's "unrestricted" strategy
+// (max_steps_per_sequence = -1) packs while anything fits: its redundant work grows with every
+// padded step until the next sequence starts.
+bool seq_fits(const std::vector<Step>& st, size_t a, size_t b, const bs_plan_options& o) {
+  if (b - a > (size_t)kMaxSeqSteps) return false;
   for (size_t k = a; k < b; ++k)
     if (has_add(st[k])) return false;
-  return seq_bytes(st, a, b, 1, 2, nullptr) <= cap;
+  SeqGeom g;
+  if (o.force_rows_per_task <= 0 && seq_geometry(st, a, b, 1, st[b - 1].out.h, 2, g) <= smem_cap(o)) return true;
+  const int64_t cap = seq_band_cap(o);
+  const int64_t R0 = o.force_rows_per_task > 0 ? o.force_rows_per_task : seq_base_rows(st[b - 1]);
+  if (seq_geometry(st, a, b, 1, R0, 2, g) > cap) return false;
+  if (o.max_steps_per_sequence != 0 || o.force_rows_per_task > 0) return true;
+  // default policy: the largest fitting band must cover its own step-0 halo
+  const int64_t Ho = st[b - 1].out.h;
+  int64_t lo = R0, hi = Ho;   // largest R in [R0, Ho] that fits (footprint grows with R)
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (seq_geometry(st, a, b, 1, mid, 2, g) <= cap) lo = mid;
+    else hi = mid - 1;
+  }
+  seq_geometry(st, a, b, 1, lo, 2, g);
+  int64_t halo = 0;
+  const size_t n = b - a;
+  for (int64_t bd = 0; bd < g.n_bands; ++bd) {   // step-0 input rows beyond the band's own share
+    const SeqRange& r0 = g.ranges[(size_t)bd * n];
+    const SeqRange& rl = g.ranges[(size_t)bd * n + n - 1];
+    const int64_t own = (st[a].in.h * (int64_t)(rl.out_hi - rl.out_lo) + Ho - 1) / Ho;
+    halo = std::max<int64_t>(halo, (r0.in_hi - r0.in_lo) - own);
+  }
+  return halo <= lo;
+}
+
+void plan_sequence(const bs_plan* p, const std::vector<Step>& steps, size_t a, size_t b, const bs_plan_options& o,
+                   Launch& l) {
+  const int64_t n_planes = steps[a].in.n * steps[a].in.c;
+  const int64_t Ho = steps[b - 1].out.h;
+  SeqGeom g;
+  if (o.force_rows_per_task <= 0 && seq_geometry(steps, a, b, 1, Ho, 2, g) <= smem_cap(o)) {
+    // whole planes: the most planes per tile that keep two CTAs per SM (else one), >= 8 tiles
+    // per CTA; up to 4 stages
+    int64_t P = 1;
+    const int64_t half = std::min<int64_t>(110 * 1024, smem_cap(o));
+    SeqGeom t;
+    while (P * 2 <= n_planes / (8 * 2 * p->num_sms) && seq_geometry(steps, a, b, P * 2, Ho, 2, t) <= half) P *= 2;
+    if (o.force_tile_planes > 0) P = o.force_tile_planes;
+    int64_t S = 2;
+    while (S < 4 && seq_geometry(steps, a, b, P, Ho, S + 1, t) <= half) ++S;
+    if (seq_geometry(steps, a, b, P, Ho, S, g) > smem_cap(o)) {
+      P = 1;
+      S = 2;
+      seq_geometry(steps, a, b, P, Ho, S, g);
+    }
+  } else {
+    // halo tiles of one plane: the largest band that fits the budget ("we increase the size of
+    // it"), or the forced band
+    const int64_t cap = seq_band_cap(o);
+    int64_t R = o.force_rows_per_task > 0 ? o.force_rows_per_task : seq_base_rows(steps[b - 1]);
+    if (o.force_rows_per_task <= 0)
+      {   // largest R in [R, Ho] that fits (the footprint grows with R)
+      int64_t lo = R, hi = Ho;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (seq_geometry(steps, a, b, 1, mid, 2, g) <= cap) lo = mid;
+        else hi = mid - 1;
+      }
+      R = lo;
+    }
+    seq_geometry(steps, a, b, 1, R, 2, g);
+    SeqGeom t;
+    if (seq_geometry(steps, a, b, 1, R, 3, t) <= cap) g = t;
+  }
+  seq_chunking(steps, a, b, g);
+  l.tile_planes = (int32_t)g.P;
+  l.stages = (int32_t)g.stages;
+  l.seq_work_floats = (int32_t)g.work_floats;
+  l.seq_bands = (int32_t)g.n_bands;
+  l.seq_band_rows = (int32_t)g.R;
+  l.seq_stage_bytes = (int32_t)g.stage_bytes;
+  l.seq_in_pitch = g.in_pitch;
+  l.seq_out_pitch = g.out_pitch;
+  l.seq_ranges = g.ranges;
 }
 
 void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& o) {
@@ -491,7 +678,7 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
   std::vector<std::pair<size_t, size_t>> seqs;
   for (size_t a = 0; a < steps.size();) {
     size_t b = a + 1;
-    while (b < steps.size() && b - a < max_steps && seq_fits(steps, a, b + 1, smem_cap(o))) ++b;
+    while (b < steps.size() && b - a < max_steps && seq_fits(steps, a, b + 1, o)) ++b;
     seqs.emplace_back(a, b);
     a = b;
   }
@@ -516,20 +703,7 @@ void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& 
       l.step.has_pool = true;
       l.step.kh = steps[a].kh; l.step.kw = steps[a].kw; l.step.sh = steps[a].sh;
       l.step.sw = steps[a].sw; l.step.ph = steps[a].ph; l.step.pw = steps[a].pw;
-      // planes per tile: the most that keep two CTAs per SM (else one), >= 8 tiles per CTA
-      const int64_t n_planes = steps[a].in.n * steps[a].in.c;
-      int64_t P = 1;
-      const int64_t half = std::min<int64_t>(110 * 1024, smem_cap(o));
-      while (P * 2 <= n_planes / (8 * 2 * p->num_sms) && seq_bytes(steps, a, b, P * 2, 2, nullptr) <= half) P *= 2;
-      if (o.force_tile_planes > 0) P = o.force_tile_planes;
-      int stages = 2;
-      while (stages < 4 && seq_bytes(steps, a, b, P, stages + 1, nullptr) <= half) ++stages;
-      if (seq_bytes(steps, a, b, P, stages, nullptr) > smem_cap(o)) { P = 1; stages = 2; }
-      int64_t wf = 0;
-      seq_bytes(steps, a, b, P, stages, &wf);
-      l.tile_planes = (int32_t)P;
-      l.stages = stages;
-      l.seq_work_floats = (int32_t)wf;
+      plan_sequence(p, steps, a, b, o, l);
     }
     p->launches.push_back(l);
   }
@@ -633,6 +807,19 @@ int ew_grid(int64_t n_elems) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n_elems + per_block - 1) / per_block, INT32_MAX / 2));
 }
 
+// A SeqArgs carrying the fields seq_smem / the occupancy query need.
+SeqArgs seq_probe(const Launch& l) {
+  SeqArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.tile_planes = l.tile_planes;
+  a.stages = l.stages;
+  a.stage_bytes = l.seq_stage_bytes;
+  a.work_floats = l.seq_work_floats;
+  a.in_plane = (int32_t)(l.step.in.h * l.step.in.w);
+  a.n_bands = l.seq_bands;
+  return a;
+}
+
 void fill_info(bs_plan* p, const std::vector<Shape4>& shapes, int n_layers, int n_inputs) {
   bs_plan_info& I = p->info;
   std::memset(&I, 0, sizeof I);
@@ -692,17 +879,17 @@ void fill_launch_info(bs_plan* p) {
       li.groups_per_warp = (int32_t)l.seq.size();          // steps fused in the sequence
       li.outputs_per_group = l.tile_planes;                 // planes per staged tile
       li.rows_per_task = (int32_t)s.out.h;
-      li.n_tasks = (n_planes + l.tile_planes - 1) / l.tile_planes;
+      li.n_tasks = (n_planes + l.tile_planes - 1) / l.tile_planes * l.seq_bands;   // tiles
       li.grid = (int)std::min<int64_t>(li.n_tasks, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
       li.block = kSeqThreads;
-      SeqArgs probe;
-      std::memset(&probe, 0, sizeof probe);
-      probe.tile_planes = l.tile_planes;
-      probe.stages = l.stages;
-      probe.work_floats = l.seq_work_floats;
-      probe.in_plane = (int32_t)(s.in.h * s.in.w);
-      li.smem_bytes = (int32_t)seq_smem(probe);
+      li.smem_bytes = (int32_t)seq_smem(seq_probe(l));
       li.tile_planes = l.tile_planes;
+      li.tile_rows = l.seq_bands > 1 ? l.seq_band_rows : 0;
+      // redundant (halo) input rows of step 0 per band: rows loaded beyond the band's own share
+      int64_t loaded = 0;
+      const size_t n = l.seq.size();
+      for (int32_t bd = 0; bd < l.seq_bands; ++bd) loaded += l.seq_ranges[(size_t)bd * n].in_hi - l.seq_ranges[(size_t)bd * n].in_lo;
+      li.halo_rows = (int32_t)(loaded - s.in.h);
       li.stages = l.stages;
     } else {
       li.groups_per_warp = l.G;
@@ -756,7 +943,10 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       a.n_planes = (img1 - img0) * s.in.c;
       a.tile_planes = l.tile_planes;
       a.stages = l.stages;
-      a.n_tiles = (a.n_planes + l.tile_planes - 1) / l.tile_planes;
+      a.n_bands = l.seq_bands;
+      a.ranges = p->seq_ranges + l.range_off;
+      a.stage_bytes = l.seq_stage_bytes;
+      a.n_tiles = (a.n_planes + l.tile_planes - 1) / l.tile_planes * l.seq_bands;
       a.work_floats = l.seq_work_floats;
       a.in_plane = (int32_t)(s.in.h * s.in.w);
       a.cdiv = make_fastdiv((uint32_t)a.C);
@@ -858,6 +1048,7 @@ void free_plan(bs_plan* p) {
     cudaSetDevice(p->device);
     if (p->params) cudaFree(p->params);
     if (p->seq_steps) cudaFree(p->seq_steps);
+    if (p->seq_ranges) cudaFree(p->seq_ranges);
     for (float* b : p->inter)
       if (b) cudaFree(b);
     for (auto& s : p->copy_stream)
@@ -899,6 +1090,9 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
   std::memset(&o, 0, sizeof o);
   o.device = -1;
   if (opts) o = *opts;
+  if (o.max_steps_per_sequence < -1)
+    return fail(BS_ERR_INVALID_ARGUMENT, "max_steps_per_sequence=%d: use -1 (unrestricted), 0 (planner) or k >= 1",
+                o.max_steps_per_sequence);
   if (o.threads_per_block != 0)
     return fail(BS_ERR_INVALID_ARGUMENT, "threads_per_block=%d: block sizes are fixed per kernel (pass 0)",
                 o.threads_per_block);
@@ -946,13 +1140,7 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
   pack_and_tile(p, steps, o);
   for (Launch& l : p->launches) {
     if (l.kernel == K_SEQ) {
-      SeqArgs probe;
-      std::memset(&probe, 0, sizeof probe);
-      probe.tile_planes = l.tile_planes;
-      probe.stages = l.stages;
-      probe.work_floats = l.seq_work_floats;
-      probe.in_plane = (int32_t)(l.step.in.h * l.step.in.w);
-      const int bps = p->host_only ? 0 : seq_max_blocks_per_sm(probe);
+      const int bps = p->host_only ? 0 : seq_max_blocks_per_sm(seq_probe(l));
       l.blocks_per_sm = bps > 0 ? bps : 1;
     } else if (l.kernel != K_EW) {
       int bps = 0;
@@ -997,10 +1185,14 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
     }
     {  // device descriptors of the on-chip sequences
       std::vector<SeqStepDev> desc;
+      std::vector<SeqRange> ranges;
       for (Launch& l : p->launches) {
         if (l.kernel != K_SEQ) continue;
         l.seq_off = desc.size();
-        for (const Step& st : l.seq) {
+        l.range_off = ranges.size();
+        ranges.insert(ranges.end(), l.seq_ranges.begin(), l.seq_ranges.end());
+        for (size_t si = 0; si < l.seq.size(); ++si) {
+          const Step& st = l.seq[si];
           SeqStepDev d;
           std::memset(&d, 0, sizeof d);
           d.H = (int32_t)st.in.h; d.W = (int32_t)st.in.w; d.Ho = (int32_t)st.out.h; d.Wo = (int32_t)st.out.w;
@@ -1013,8 +1205,9 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
           d.pro = make_prog(p, st.pro);
           d.epi = make_prog(p, st.epi);
           d.epi_class = prog_class(st.epi);
-          d.fast = st.has_pool && st.is_max && st.kh == 3 && st.kw == 3 && st.sh == 1 && st.sw == 1 &&
-                   st.ph == 1 && st.pw == 1 && st.pro.empty() && d.epi_class != PC_GENERIC;
+          d.fast = is_fast_step(st) ? 1 : 0;
+          d.in_pitch = l.seq_in_pitch[si];
+          d.out_pitch = l.seq_out_pitch[si];
           desc.push_back(d);
         }
       }
@@ -1024,6 +1217,11 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
         if ((e = cudaMemcpy(p->seq_steps, desc.data(), desc.size() * sizeof(SeqStepDev), cudaMemcpyHostToDevice)) !=
             cudaSuccess)
           return cuda_fail("cudaMemcpy(sequence steps)", e);
+        if ((e = cudaMalloc(&p->seq_ranges, ranges.size() * sizeof(SeqRange))) != cudaSuccess)
+          return cuda_fail("cudaMalloc(sequence ranges)", e);
+        if ((e = cudaMemcpy(p->seq_ranges, ranges.data(), ranges.size() * sizeof(SeqRange), cudaMemcpyHostToDevice)) !=
+            cudaSuccess)
+          return cuda_fail("cudaMemcpy(sequence ranges)", e);
       }
     }
     int64_t inter = 0;

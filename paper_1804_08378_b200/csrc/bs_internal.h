@@ -89,25 +89,41 @@ enum KernelKind : int32_t { K_EW = 1, K_POOL_SPEC = 2, K_POOL_GENERIC = 3, K_POO
 // One step of an on-chip sequence: [prologue] pool [epilogue] on the
 // step's input planes (H x W) -> (Ho x Wo).  A step without a pool is a 1x1/s1 max pool
 // (the identity).  Held in a plan-owned device array; programs have no ADD ops.
-constexpr int kMaxSeqSteps = 16;
+// A device-table limit (the descriptors of a sequence live in a per-CTA shared table); the
+// planner's real limit is the shared-memory footprint of the sequence's tile.
+constexpr int kMaxSeqSteps = 64;
 struct SeqStepDev {
   int32_t H, W, Ho, Wo;
   int32_t kh, kw, sh, sw, ph, pw;
   int32_t is_max, count_include_pad;
-  int32_t fast;             // 1: 3x3/s1/p1 max pool, no prologue, epilogue class <= PC_AFFINE_RELU
+  int32_t fast;             // 1: 3x3/s1/p1 max pool, no prologue, epilogue class <= PC_AFFINE_RELU,
+                            //    W % 4 == 0, W <= 256 (vectorised path, k_seq.cu)
   int32_t epi_class;        // ProgClass of epi
+  int32_t in_pitch;         // floats per plane in the step's input buffer (stage or work buffer)
+  int32_t out_pitch;        // floats per plane in the step's output work buffer (unused by the last step)
   OpProgram pro, epi;
+};
+// Rows of one step for one band of a tile (the sequence's halo back-propagation):
+// the input buffer holds rows [in_lo, in_hi) of the step's input plane, the step computes rows
+// [out_lo, out_hi) of its output; the fast path splits those rows into n_chunks chunks of L rows.
+struct SeqRange {
+  int32_t in_lo, in_hi, out_lo, out_hi;
+  int32_t n_chunks, L;
+  FastDiv chunks;           // division by n_chunks
 };
 struct SeqArgs {
   const float* in;          // sequence input base (plane 0)
   float* out;               // sequence output base (plane 0)
   const SeqStepDev* steps;  // device array of n_steps descriptors
+  const SeqRange* ranges;   // device array [n_bands][n_steps]
   int32_t n_steps;
   int32_t C;
   int64_t plane0, n_planes;
   int32_t tile_planes, stages;
-  int64_t n_tiles;
-  int32_t work_floats;      // floats per work buffer (tile_planes x largest intermediate plane)
+  int32_t n_bands;          // 1: whole-plane tiles; > 1: row-band tiles of one plane (halo tiles)
+  int64_t n_tiles;          // ceil(n_planes / tile_planes) * n_bands
+  int32_t stage_bytes;      // bytes per ring stage (128-B multiple)
+  int32_t work_floats;      // floats per work buffer
   int32_t in_plane;         // H0 * W0
   FastDiv cdiv;             // channels C (plane -> channel)
 };

@@ -82,11 +82,12 @@ def test_step_counts(bs, layers, steps):
     assert bs.bs_plan_query(p)["n_steps"] == steps
 
 
-@pytest.mark.parametrize("depth,policy,seqs", [(16, 5, 4), (16, 1, 16), (16, 0, 1), (40, 0, 3), (40, 5, 8),
-                                               (1, 0, 1)])
+@pytest.mark.parametrize("depth,policy,seqs", [(16, 5, 4), (16, 1, 16), (16, 0, 1), (40, 0, 1), (40, 5, 8),
+                                               (1, 0, 1), (70, 0, 2)])
 def test_sequence_packing(bs, depth, policy, seqs):
     """§5.1 blocks [MaxPool3x3/s1/p1, BN, ReLU] x depth: one step per block; the paper's three
-    policies -> ceil(depth / limit) sequences (16 blocks, <= 5 -> 4)."""
+    policies -> ceil(depth / limit) sequences (16 blocks, <= 5 -> 4).  Whole
+    28x28 planes need no halo, so "unrestricted" is limited only by the 64-step device table."""
     layers = []
     for b in range(depth):
         layers += [synth.maxpool(3, 1, 1), synth.batchnorm(8, b), synth.relu()]
@@ -94,13 +95,56 @@ def test_sequence_packing(bs, depth, policy, seqs):
     assert info["n_steps"] == depth and info["n_sequences"] == seqs and info["n_launches"] == seqs
 
 
-def test_sequence_respects_shared_memory(bs):
-    """Planes too large for shared memory are not fused (one step per sequence)."""
+def test_large_planes_use_halo_tiles(bs):
+    """Planes too large to hold whole in shared memory are fused with halo (row-band) tiles."""
     layers = [synth.maxpool(3, 1, 1), synth.relu(), synth.maxpool(3, 1, 1)]
-    info = bs.bs_plan_query(host_plan(bs, layers, (1, 2, 224, 224)))
-    assert info["n_sequences"] == 2
-    info = bs.bs_plan_query(host_plan(bs, layers, (1, 2, 56, 56)))
-    assert info["n_sequences"] == 1
+    p = host_plan(bs, layers, (1, 2, 224, 224))
+    info = bs.bs_plan_query(p)
+    li = bs.bs_plan_query_launch(p, 0)
+    assert info["n_sequences"] == 1 and li["kernel_name"] == "sequence_staged_tma"
+    assert 0 < li["tile_rows"] < 224 and li["halo_rows"] > 0
+    p = host_plan(bs, layers, (1, 2, 56, 56))
+    li = bs.bs_plan_query_launch(p, 0)
+    assert bs.bs_plan_query(p)["n_sequences"] == 1 and li["tile_rows"] == 0 and li["halo_rows"] == 0
+
+
+def _sec51_split_depth(W, H, budget=110 * 1024, lanes=256):
+    """Independent closed form of the paper's packing rule for §5.1 blocks on H x W
+    planes with halo tiles: base tile = ceil(256 / W) output rows (one output per consumer lane),
+    each 3x3/s1/p1 block adds one input row above and below; the sequence footprint is two ring
+    stages of step 0's input band + two work buffers of the largest intermediate band (fp32)
+    + 128 B of barriers + 1 KB slack.  Returns the most blocks one sequence holds."""
+    r0 = -(-lanes // W)
+    d = 1
+    while True:
+        n = d + 1
+        rows_in = min(H, r0 + 2 * n)                 # step 0's input band for n blocks
+        rows_mid = min(H, r0 + 2 * (n - 1))          # the largest intermediate (step 0's output)
+        stage = -(-(rows_in * W * 4 + 16) // 128) * 128
+        work = -(-(rows_mid * W) // 4) * 4 * 4
+        if 128 + 2 * stage + 2 * work + 1024 > budget:
+            return d
+        d = n
+
+
+@pytest.mark.parametrize("H,depth", [(224, 40), (112, 70), (160, 40)])
+def test_halo_sequence_split_depth(bs, H, depth):
+    """'Unrestricted' (-1) §5.1 networks on large planes split where the growing halo band overflows
+    the shared-memory budget (the paper's cache-limit artifacts), at the depth the
+    closed form gives -- not at a fixed step limit."""
+    layers = []
+    for b in range(depth):
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(4, b), synth.relu()]
+    p = host_plan(bs, layers, (2, 4, H, H), max_steps_per_sequence=-1)
+    info = bs.bs_plan_query(p)
+    d = _sec51_split_depth(H, H)
+    whole = 128 + 2 * (-(-(H * H * 4 + 16) // 128) * 128) + 2 * H * H * 4 + 1024 <= 220 * 1024
+    if whole:
+        assert info["n_sequences"] == -(-depth // 64)
+        return
+    assert info["n_sequences"] == -(-depth // d), (d, info)
+    li = bs.bs_plan_query_launch(p, 0)
+    assert li["groups_per_warp"] == d and li["tile_rows"] >= -(-256 // H)
 
 
 def test_copy_is_elided(bs):
@@ -273,8 +317,13 @@ def test_smem_budget_option(bs):
     drop to fewer stages or to the global-memory walker (the paper's cache budget)."""
     sec = synth.synthetic51(4, batch=2, C=3, H=56)
     assert bs.bs_plan_query(host_plan(bs, sec.layers, sec.shape))["n_launches"] == 1
+    # 40 KB: whole 56x56 planes no longer fit -> halo tiles, split where the closed form says
     small = bs.bs_plan_create(sec.layers, sec.shape, {"host_only": 1, "smem_budget_bytes": 40 * 1024})
-    assert bs.bs_plan_query(small)["n_launches"] == 4
+    d = _sec51_split_depth(56, 56, budget=40 * 1024)
+    assert bs.bs_plan_query(small)["n_launches"] == -(-4 // d)
+    assert bs.bs_plan_query_launch(small, 0)["tile_rows"] > 0
+    tiny = bs.bs_plan_create(sec.layers, sec.shape, {"host_only": 1, "smem_budget_bytes": 4 * 1024})
+    assert bs.bs_plan_query(tiny)["n_launches"] == 4            # not even a 2-block band fits
     s1 = synth.workload("alexnet")[0]
     assert bs.bs_plan_query_launch(host_plan(bs, s1.layers, s1.shape), 0)["kernel"] == 6
     p = bs.bs_plan_create(s1.layers, s1.shape, {"host_only": 1, "smem_budget_bytes": 40 * 1024})
@@ -297,3 +346,32 @@ def test_wide_plane_plans(bs, shape, layers):
     assert li["outputs_per_group"] * -(-Wo // li["outputs_per_group"]) >= Wo
     assert li["tile_planes"] >= 1 and li["stages"] >= 2
     assert li["smem_bytes"] >= 128 + li["stages"] * li["tile_planes"] * shape[2] * shape[3] * 4
+
+
+@pytest.mark.parametrize("H", [224, 160, 300])
+def test_default_policy_bounds_halo(bs, H):
+    """The planner's default (0) stops a halo-tiled sequence once the band no longer covers its
+    own input halo: every sequence has halo rows <= band rows per band, and one more step would
+    break that (or not fit)."""
+    depth = 40
+    layers = []
+    for b in range(depth):
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(4, b), synth.relu()]
+    p = host_plan(bs, layers, (2, 4, H, H))
+    info = bs.bs_plan_query(p)
+    assert 1 < info["n_sequences"] < depth
+    for k in range(info["n_launches"]):
+        li = bs.bs_plan_query_launch(p, k)
+        if li["kernel_name"] != "sequence_staged_tma" or li["tile_rows"] == 0:
+            continue
+        n_bands = -(-H // li["tile_rows"])
+        assert li["halo_rows"] <= n_bands * li["tile_rows"], li
+        assert 2 * li["groups_per_warp"] <= li["tile_rows"] + 2, li   # 2 halo rows per 3x3/p1 step
+    unres = bs.bs_plan_query(host_plan(bs, layers, (2, 4, H, H), max_steps_per_sequence=-1))
+    assert unres["n_sequences"] <= info["n_sequences"]
+
+
+def test_policy_validation(bs):
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_plan_create([synth.relu()], (1, 1, 4, 4), {"host_only": 1, "max_steps_per_sequence": -2})
+    assert e.value.status == 2

@@ -1,0 +1,118 @@
+"""GPU parity of on-chip multi-step sequences (NEXT-2, k_seq.cu) against the oracle: the vectorised
+3x3/s1/p1 fast path at every segment geometry, halo (row-band) tiles on planes too large to hold
+whole, and tile invariance: the result does not depend on the
+band height or the planes per tile -- bit for bit, since every output element gets
+the same arithmetic in the same order whatever the tiling."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests import _util as U
+
+pytestmark = pytest.mark.gpu
+
+
+def _bs():
+    import paper_1804_08378_b200 as bs
+    return bs
+
+
+def run_gpu(layers, x, opts=None):
+    bs = _bs()
+    plan = bs.bs_plan_create(layers, x.shape, opts)
+    out = torch.full(bs.bs_plan_query(plan)["out"], float("nan"), device="cuda")
+    bs.bs_execute(plan, torch.from_numpy(np.ascontiguousarray(x)).cuda(), out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), plan
+
+
+def sec51(depth, C, signed=False, last_plain=False):
+    layers = []
+    for b in range(depth):
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(C, 700 + b, signed_gamma=signed and b % 2 == 1), synth.relu()]
+    if last_plain:
+        layers += [synth.maxpool(3, 1, 1)]
+    return layers
+
+
+@pytest.mark.parametrize("W", [4, 8, 28, 56, 60, 64, 68, 100, 128, 132, 200, 252, 256])
+def test_fast_path_widths(W, cuda_dev, oracle_lib):
+    """Segments of 16 lanes (W <= 64), 32 lanes x 1 (<= 128), 32 lanes x 2 (<= 256)."""
+    bs = _bs()
+    shape = (2, 3, 23, W)
+    layers = sec51(4, 3, signed=True, last_plain=True)
+    x = synth.uniform_np(W, int(np.prod(shape))).reshape(shape)
+    ref = oracle.run_bf(layers, x)
+    for opts in (None, {"force_tile_planes": 1}, {"force_rows_per_task": 5}, {"force_rows_per_task": 1}):
+        got, plan = run_gpu(layers, x, opts)
+        assert bs.bs_plan_query(plan)["n_launches"] == 1
+        U.assert_close(got, ref, f"W={W} {opts}")
+
+
+def test_tile_invariance_bitexact(cuda_dev, oracle_lib):
+    bs = _bs()
+    shape = (2, 4, 61, 96)
+    layers = sec51(6, 4, signed=True)
+    x = synth.uniform_np(5, int(np.prod(shape))).reshape(shape)
+    ref = oracle.run_bf(layers, x)
+    base, _ = run_gpu(layers, x)
+    U.assert_close(base, ref, "whole planes")
+    for opts in ({"force_rows_per_task": 1}, {"force_rows_per_task": 2}, {"force_rows_per_task": 7},
+                 {"force_rows_per_task": 30}, {"force_tile_planes": 1}, {"force_tile_planes": 3},
+                 {"max_steps_per_sequence": 1}, {"max_steps_per_sequence": 4}):
+        got, plan = run_gpu(layers, x, opts)
+        U.assert_bitexact(got, base, f"{opts}")
+    li = bs.bs_plan_query_launch(run_gpu(layers, x, {"force_rows_per_task": 7})[1], 0)
+    assert li["tile_rows"] == 7 and li["halo_rows"] > 0
+
+
+def test_halo_generic_steps(cuda_dev, oracle_lib):
+    """Halo tiles through generic steps: odd widths, avg pools with padding, strided pools, prologues."""
+    shape = (2, 3, 77, 53)
+    layers = [synth.maxpool(3, 1, 1), synth.relu(), synth.avgpool(3, 1, 1), synth.batchnorm(3, 5, signed_gamma=True),
+              synth.maxpool(3, 2, 1), synth.scale(-1.5), synth.relu(), synth.maxpool(3, 1, 1), synth.avgpool(2, 2),
+              synth.batchnorm(3, 6), synth.maxpool((3, 1), (1, 1), (1, 0))]
+    x = synth.uniform_np(9, int(np.prod(shape))).reshape(shape)
+    ref = oracle.run_bf(layers, x)
+    base, plan = run_gpu(layers, x)
+    U.assert_close(base, ref, "default")
+    for R in (1, 2, 3, 5, 9):
+        got, plan = run_gpu(layers, x, {"force_rows_per_task": R})
+        assert _bs().bs_plan_query_launch(plan, 0)["tile_rows"] in (R, 0)
+        U.assert_bitexact(got, base, f"rows {R}")
+
+
+@pytest.mark.parametrize("H,depth", [(224, 20), (150, 33), (112, 40)])
+def test_sec51_large_planes(H, depth, cuda_dev, oracle_lib):
+    """§5.1 networks on planes too large to stage whole (default budget): halo tiles, split where
+    the band overflows the budget; every policy gives the same bits."""
+    bs = _bs()
+    shape = (2, 3, H, H)
+    layers = sec51(depth, 3)
+    x = synth.uniform_np(H + depth, int(np.prod(shape))).reshape(shape)
+    ref = oracle.run_bf(layers, x)
+    outs = []
+    for policy in (0, 5, 1, -1):
+        got, plan = run_gpu(layers, x, {"max_steps_per_sequence": policy})
+        U.assert_close(got, ref, f"H={H} depth {depth} policy {policy}")
+        outs.append(got)
+    for k, name in ((1, "5"), (2, "1"), (3, "unrestricted")):
+        U.assert_bitexact(outs[k], outs[0], f"policy {name} vs planner")
+
+
+@pytest.mark.parametrize("shape,depth", [((32, 64, 224, 224), 16), ((64, 64, 112, 112), 24), ((128, 64, 56, 56), 40)])
+def test_sec51_full_shapes_sampled(shape, depth, cuda_dev, oracle_lib):
+    """The §5.1 benchmark shapes (R15) at the depths exp_sec51.py times, unrestricted
+    policy; images checked against the oracle one by one."""
+    bs = _bs()
+    case = synth.synthetic51(depth, batch=shape[0], C=shape[1], H=shape[2])
+    x = synth.uniform_torch(case.input_seed, case.shape, device="cuda")
+    plan = bs.bs_plan_create(case.layers, case.shape)
+    out = torch.empty(bs.bs_plan_query(plan)["out"], device="cuda")
+    bs.bs_execute(plan, x, out)
+    torch.cuda.synchronize()
+    for n in (0, shape[0] - 1):
+        ref = oracle.run_bf(case.layers, x[n:n + 1].cpu().numpy())
+        U.check(out[n:n + 1].cpu().numpy(), ref, case.layers, f"{shape} image {n}")
