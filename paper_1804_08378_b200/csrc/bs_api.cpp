@@ -99,6 +99,7 @@ struct Launch {
   int32_t seq_bands = 1;            // K_SEQ: row bands per plane (1 = whole-plane tiles)
   int32_t seq_band_rows = 0;        // K_SEQ: output rows of the last step per band
   int32_t seq_stage_bytes = 0;      // K_SEQ: bytes per ring stage
+  int32_t seq_inplace_seg = 0;      // K_SEQ: > 0 = the warp-per-plane in-place kernel (lane segment width)
   std::vector<int32_t> seq_in_pitch, seq_out_pitch;   // K_SEQ: floats per plane, per step
   std::vector<SeqRange> seq_ranges; // K_SEQ: [bands][steps]
   std::vector<HostOp> dev_pro, dev_epi;  // programs as the kernel runs them
@@ -478,8 +479,9 @@ bool has_add(const Step& s) {
 // every step are back-propagated through the windows (in_lo = out_lo*s - p,
 // in_hi = (out_hi-1)*s + k - p, clipped to the plane): a step computes the rows the next step
 // needs, so a band's input grows by the window overlap of every step -- the paper's redundant
-// halo work.  Shared memory = ring stages of step 0's input rows + two work buffers
-// of the largest intermediate band (the paper's "two buffers").
+// halo work.  Shared memory = ring stages of step 0's input rows + one work buffer:
+// a tile's steps ping-pong between its stage and the work buffer (the paper's "two buffers",
+// P:L613-615), so the stage is held until the tile's last step.
 struct SeqGeom {
   int64_t P = 1, R = 0, n_bands = 1, stages = 2;
   int64_t stage_bytes = 0, work_floats = 0, smem = 0;
@@ -531,8 +533,10 @@ int64_t seq_geometry(const std::vector<Step>& st, size_t a, size_t b, int64_t P,
     rows_in[k] = std::max<int64_t>(rows_in[k], r.in_hi - r.in_lo);
     rows_out[k] = std::max<int64_t>(rows_out[k], r.out_hi - r.out_lo);
   }
+  // steps ping-pong between the tile's stage and ONE work buffer (k_seq.cu): even steps write the
+  // work buffer, odd steps the stage, which must also hold those intermediates
   const int64_t W0 = st[a].in.w;
-  g.stage_bytes = (P * rows_in[0] * W0 * 4 + 16 + 127) / 128 * 128;
+  int64_t stage = P * rows_in[0] * W0 * 4 + 16;
   g.in_pitch.assign(n, 0);
   g.out_pitch.assign(n, 0);
   g.in_pitch[0] = (int32_t)(g.n_bands == 1 ? st[a].in.h * W0 : rows_in[0] * W0);
@@ -541,10 +545,14 @@ int64_t seq_geometry(const std::vector<Step>& st, size_t a, size_t b, int64_t P,
     const int64_t pitch = (rows_out[k] * st[a + k].out.w + 3) / 4 * 4;
     g.out_pitch[k] = (int32_t)pitch;
     g.in_pitch[k + 1] = (int32_t)pitch;
-    wf = std::max(wf, P * pitch);
+    if (k % 2 == 0) wf = std::max(wf, P * pitch);
+    else stage = std::max(stage, P * pitch * 4);
   }
+  g.stage_bytes = (stage + 127) / 128 * 128;
   g.work_floats = wf;
-  g.smem = 128 + S * g.stage_bytes + 2 * wf * 4 + 1024;
+  // + per-tile tables (k_seq.cu seq_table_bytes): ranges of every step, (scale, shift) per (step, plane)
+  const int64_t tables = ((int64_t)n * (int64_t)sizeof(SeqRange) + (int64_t)n * P * 8 + 127) / 128 * 128;
+  g.smem = 128 + S * g.stage_bytes + wf * 4 + tables + 1024;
   return g.smem;
 }
 
@@ -580,6 +588,27 @@ int64_t seq_band_cap(const bs_plan_options& o) {
 // last step's output that give each of the 256 consumer lanes an output.
 int64_t seq_base_rows(const Step& last) { return std::max<int64_t>(1, (256 + last.out.w - 1) / last.out.w); }
 
+// Dynamic smem of the in-place kernel for [a, b), or -1 if it does not apply / fit.
+int64_t inplace_smem(const std::vector<Step>& steps, size_t a, size_t b, const bs_plan_options& o,
+                     int64_t* stage_out = nullptr, int64_t* stages_out = nullptr, int64_t* planes_out = nullptr) {
+  if (o.force_tile_planes > 0 || o.force_rows_per_task > 0 || b - a > (size_t)kMaxSeqSteps) return -1;
+  const int64_t W = steps[a].in.w, H = steps[a].in.h;
+  if (W > 128) return -1;
+  for (size_t k = a; k < b; ++k)
+    if (!is_fast_step(steps[k]) || steps[k].in.w != W || steps[k].in.h != H) return -1;
+  // planes per CTA: warps per plane chosen so that ~4 CTAs (16 consumer warps) fit an SM: small
+  // planes one warp each, 112 x 112 planes four warps each
+  int64_t P = kInplaceWarps;
+  while (P > 1 && 4 * (P * H * W * 4 + 2048) > 220 * 1024) P /= 2;
+  const int64_t stage = (P * H * W * 4 + 16 + 127) / 128 * 128;
+  const int64_t S = o.force_stages >= 1 ? std::min<int64_t>(kStagedMaxStages, o.force_stages) : 1;
+  const int64_t smem = 128 + S * stage + (int64_t)kInplaceWarps * (int64_t)(b - a) * 8 + 1024;
+  if (stage_out) *stage_out = stage;
+  if (stages_out) *stages_out = S;
+  if (planes_out) *planes_out = P;
+  return smem <= smem_cap(o) ? smem : -1;
+}
+
 // a4 sequence packing: greedily add the next step while the sequence's
 // tile still fits the shared-memory budget -- whole planes, else a halo band of the base tile
 // size whose input grows with every added padded step -- and the policy's step limit allows it.
@@ -594,6 +623,7 @@ bool seq_fits(const std::vector<Step>& st, size_t a, size_t b, const bs_plan_opt
   if (b - a > (size_t)kMaxSeqSteps) return false;
   for (size_t k = a; k < b; ++k)
     if (has_add(st[k])) return false;
+  if (inplace_smem(st, a, b, o) >= 0) return true;   // whole planes, in place (k_seq.cu seq_inplace)
   SeqGeom g;
   if (o.force_rows_per_task <= 0 && seq_geometry(st, a, b, 1, st[b - 1].out.h, 2, g) <= smem_cap(o)) return true;
   const int64_t cap = seq_band_cap(o);
@@ -620,10 +650,34 @@ bool seq_fits(const std::vector<Step>& st, size_t a, size_t b, const bs_plan_opt
   return halo <= lo;
 }
 
+// The warp-per-plane in-place kernel (k_seq.cu seq_inplace) takes sequences made only of fast
+// steps on whole planes of W <= 128: each consumer warp owns one plane for the whole sequence (no
+// CTA barrier, no work buffer); one stage per CTA by default, so several CTAs share an SM.
+bool plan_inplace(const std::vector<Step>& steps, size_t a, size_t b, const bs_plan_options& o, Launch& l) {
+  int64_t stage = 0, S = 0, P = 0;
+  if (inplace_smem(steps, a, b, o, &stage, &S, &P) < 0) return false;
+  const int64_t W = steps[a].in.w, H = steps[a].in.h;
+  const int seg = W <= 64 ? 16 : 32;
+  l.seq_inplace_seg = seg;
+  l.tile_planes = (int32_t)P;
+  l.stages = (int32_t)S;
+  l.seq_stage_bytes = (int32_t)stage;
+  l.seq_work_floats = 0;
+  l.seq_bands = 1;
+  l.seq_band_rows = (int32_t)H;
+  SeqGeom g;   // whole-plane ranges (unused by the kernel; kept for the launch info)
+  seq_geometry(steps, a, b, 1, H, 2, g);
+  l.seq_in_pitch = g.in_pitch;
+  l.seq_out_pitch = g.out_pitch;
+  l.seq_ranges = g.ranges;
+  return true;
+}
+
 void plan_sequence(const bs_plan* p, const std::vector<Step>& steps, size_t a, size_t b, const bs_plan_options& o,
                    Launch& l) {
   const int64_t n_planes = steps[a].in.n * steps[a].in.c;
   const int64_t Ho = steps[b - 1].out.h;
+  if (plan_inplace(steps, a, b, o, l)) return;
   SeqGeom g;
   if (o.force_rows_per_task <= 0 && seq_geometry(steps, a, b, 1, Ho, 2, g) <= smem_cap(o)) {
     // whole planes: the most planes per tile that keep two CTAs per SM (else one), >= 8 tiles
@@ -817,6 +871,8 @@ SeqArgs seq_probe(const Launch& l) {
   a.work_floats = l.seq_work_floats;
   a.in_plane = (int32_t)(l.step.in.h * l.step.in.w);
   a.n_bands = l.seq_bands;
+  a.n_steps = (int32_t)l.seq.size();
+  a.inplace_seg = l.seq_inplace_seg;
   return a;
 }
 
@@ -881,8 +937,8 @@ void fill_launch_info(bs_plan* p) {
       li.rows_per_task = (int32_t)s.out.h;
       li.n_tasks = (n_planes + l.tile_planes - 1) / l.tile_planes * l.seq_bands;   // tiles
       li.grid = (int)std::min<int64_t>(li.n_tasks, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
-      li.block = kSeqThreads;
-      li.smem_bytes = (int32_t)seq_smem(seq_probe(l));
+      li.block = l.seq_inplace_seg ? 32 * (kInplaceWarps + 1) : kSeqThreads;
+      li.smem_bytes = (int32_t)(l.seq_inplace_seg ? seq_inplace_smem(seq_probe(l)) : seq_smem(seq_probe(l)));
       li.tile_planes = l.tile_planes;
       li.tile_rows = l.seq_bands > 1 ? l.seq_band_rows : 0;
       // redundant (halo) input rows of step 0 per band: rows loaded beyond the band's own share
@@ -948,6 +1004,7 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       a.stage_bytes = l.seq_stage_bytes;
       a.n_tiles = (a.n_planes + l.tile_planes - 1) / l.tile_planes * l.seq_bands;
       a.work_floats = l.seq_work_floats;
+      a.inplace_seg = l.seq_inplace_seg;
       a.in_plane = (int32_t)(s.in.h * s.in.w);
       a.cdiv = make_fastdiv((uint32_t)a.C);
       const int grid = (int)std::min<int64_t>(a.n_tiles, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);

@@ -110,6 +110,7 @@ struct SeqRange {
   int32_t in_lo, in_hi, out_lo, out_hi;
   int32_t n_chunks, L;
   FastDiv chunks;           // division by n_chunks
+  int32_t pad_;             // 40 bytes: the float2 table after an array of these stays 8-B aligned
 };
 struct SeqArgs {
   const float* in;          // sequence input base (plane 0)
@@ -126,9 +127,13 @@ struct SeqArgs {
   int32_t work_floats;      // floats per work buffer
   int32_t in_plane;         // H0 * W0
   FastDiv cdiv;             // channels C (plane -> channel)
+  int32_t inplace_seg;      // > 0: the warp-per-plane in-place kernel (seq_inplace) with lane
+                            // segments of this width (16 or 32); 0: seq_staged
 };
+constexpr int kInplaceWarps = 4;   // consumer warps per CTA of seq_inplace (1, 2 or 4 per plane)
 cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st);
 size_t seq_smem(const SeqArgs& a);
+size_t seq_inplace_smem(const SeqArgs& a);
 int seq_max_blocks_per_sm(const SeqArgs& a);
 
 // Launchers (k_*.cu).  Return the launch error (cudaSuccess on success).

@@ -31,9 +31,18 @@ namespace bs {
 //    so padding stays absent.  Outputs: STS.128 to the next work buffer, STG.128 from the last.
 //  * generic: lane = output column, a windowed interpreter (any pool, prologue, epilogue).
 
+// Per-tile tables in shared memory: the tile's row ranges of every step and the folded BN
+// (scale, shift) of every (step, plane) -- loaded once per tile, all at once, instead of one
+// dependent global load per step.
+__host__ __device__ inline size_t seq_table_bytes(int n_steps, int tile_planes) {
+  return ((size_t)n_steps * sizeof(SeqRange) + (size_t)n_steps * tile_planes * sizeof(float2) + 127) / 128 * 128;
+}
+
 size_t seq_smem(const SeqArgs& a) {
-  // barriers | stages | 2 work buffers | 1 KB slack (vector loads of idle lanes past a row end)
-  return 128 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)a.work_floats * 4 + 1024;
+  // barriers | stages | work buffer | per-tile tables | 1 KB slack (vector loads of idle lanes
+  // past a row end)
+  return 128 + (size_t)a.stages * a.stage_bytes + (size_t)a.work_floats * 4 +
+         seq_table_bytes(a.n_steps, a.tile_planes) + 1024;
 }
 
 // One output element of a generic step from a smem plane holding rows [in_lo, ...) (padding
@@ -88,8 +97,7 @@ __device__ __forceinline__ void sts128(uint32_t a, const float4& v) {
 // column segment) are dealt to the warps; a SEG = 16 warp walks two at once (one per half).
 template <int SEG, int NSEG, bool LAST, int EPI>
 __device__ __forceinline__ void seq_fast_step(const SeqStepSm& f, const SeqRange& rg, uint32_t in_s, uint32_t out_s,
-                                              float* gout, int np, uint32_t plane_base, const FastDiv& cdiv, int C,
-                                              int cw, int lane) {
+                                              float* gout, int np, const float2* taff, int cw, int lane) {
   constexpr int PER_WARP = 32 / SEG;
   const int W = f.W;
   const int sl = lane & (SEG - 1), half = lane / SEG;
@@ -109,16 +117,10 @@ __device__ __forceinline__ void seq_fast_step(const SeqStepSm& f, const SeqRange
     const bool col_ok = c < W;
     const int r0 = rg.out_lo + chk * rg.L;
     const int r1 = min(rg.out_hi, r0 + rg.L);
-    float2 aff = make_float2(1.f, 0.f);
-    if (EPI >= 2) {
-      const uint32_t plane = plane_base + (uint32_t)p;
-      const int ch = (int)(plane - fdiv(plane, cdiv) * (uint32_t)C);
-      aff = __ldg(f.aff + ch);
-    }
+    const float2 aff = EPI >= 2 ? taff[p] : make_float2(1.f, 0.f);
     const uint32_t rowbase = in_s + 4u * (uint32_t)(p * f.in_pitch + c);
-    auto hrow = [&](int r) -> float4 {
-      r = min(max(r, lo_c), hi_c);
-      const uint32_t ad = rowbase + (uint32_t)(r - rg.in_lo) * W4;
+    // horizontal 3-max of the row at shared address ad (4 columns of this lane)
+    auto hrow = [&](uint32_t ad) -> float4 {
       const float4 x = lds128(ad);
       float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
       float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
@@ -135,48 +137,63 @@ __device__ __forceinline__ void seq_fast_step(const SeqStepSm& f, const SeqRange
       if (EPI == 1 || EPI == 3) v = relu(v);
       return v;
     };
-    float4 hA = hrow(r0 - 1), hB = hrow(r0);
+    // rows r0-1 and r0 prime the window (clamped at the plane's top edge: a duplicate row); rows
+    // r0+1 .. r0+L are streamed, only the last of them can pass the bottom edge (clamped by an
+    // address select).  Three row registers rotate through an unrolled-by-3 loop (no moves).
+    const uint32_t ad0 = rowbase + (uint32_t)(r0 - rg.in_lo) * W4;
+    float4 hA = hrow(r0 - 1 >= lo_c ? ad0 - W4 : ad0);
+    float4 hB = hrow(ad0);
+    float4 hC;
+    uint32_t ad = ad0;
+    const uint32_t ad_last = rowbase + (uint32_t)(hi_c - rg.in_lo) * W4;   // the bottom input row
     float* og = LAST ? gout + (size_t)p * ((size_t)f.H * W) + (size_t)r0 * W + c : nullptr;
     uint32_t os = out_s + 4u * (uint32_t)(p * f.out_pitch + (r0 - rg.out_lo) * W + c);
     const bool st_ok = item_ok && col_ok;
-#pragma unroll 2
-    for (int i = 0; i < rg.L; ++i) {
-      const float4 hC = hrow(r0 + i + 1);
+    const int n_ok = st_ok ? r1 - r0 : 0;    // rows this lane stores
+    auto row = [&](int i, const float4& a, const float4& b, float4& nx) {
+      ad += W4;
+      nx = hrow(min(ad, ad_last));
       float4 o;
-      o.x = epi(max3f(hA.x, hB.x, hC.x));
-      o.y = epi(max3f(hA.y, hB.y, hC.y));
-      o.z = epi(max3f(hA.z, hB.z, hC.z));
-      o.w = epi(max3f(hA.w, hB.w, hC.w));
-      if (st_ok && r0 + i < r1) {
+      o.x = epi(max3f(a.x, b.x, nx.x));
+      o.y = epi(max3f(a.y, b.y, nx.y));
+      o.z = epi(max3f(a.z, b.z, nx.z));
+      o.w = epi(max3f(a.w, b.w, nx.w));
+      if (i < n_ok) {
         if (LAST) st_stream4(og, o);
         else sts128(os, o);
       }
       if (LAST) og += W;
       else os += W4;
-      hA = hB;
-      hB = hC;
+    };
+    int i = 0;
+    for (; i + 3 <= rg.L; i += 3) {
+      row(i, hA, hB, hC);
+      row(i + 1, hB, hC, hA);
+      row(i + 2, hC, hA, hB);
+    }
+    if (i < rg.L) {
+      row(i, hA, hB, hC);
+      if (i + 1 < rg.L) row(i + 1, hB, hC, hA);
     }
   }
 }
 
 template <bool LAST, int EPI>
 __device__ __forceinline__ void seq_fast_paths(const SeqStepSm& f, const SeqRange& rg, uint32_t in_s, uint32_t out_s,
-                                               float* gout, int np, uint32_t pb, const FastDiv& cdiv, int C, int cw,
-                                               int lane) {
-  if (f.path == 1) seq_fast_step<16, 1, LAST, EPI>(f, rg, in_s, out_s, gout, np, pb, cdiv, C, cw, lane);
-  else if (f.path == 2) seq_fast_step<32, 1, LAST, EPI>(f, rg, in_s, out_s, gout, np, pb, cdiv, C, cw, lane);
-  else seq_fast_step<32, 2, LAST, EPI>(f, rg, in_s, out_s, gout, np, pb, cdiv, C, cw, lane);
+                                               float* gout, int np, const float2* taff, int cw, int lane) {
+  if (f.path == 1) seq_fast_step<16, 1, LAST, EPI>(f, rg, in_s, out_s, gout, np, taff, cw, lane);
+  else if (f.path == 2) seq_fast_step<32, 1, LAST, EPI>(f, rg, in_s, out_s, gout, np, taff, cw, lane);
+  else seq_fast_step<32, 2, LAST, EPI>(f, rg, in_s, out_s, gout, np, taff, cw, lane);
 }
 
 template <bool LAST>
 __device__ __forceinline__ void seq_fast(const SeqStepSm& f, const SeqRange& rg, uint32_t in_s, uint32_t out_s,
-                                         float* gout, int np, uint32_t pb, const FastDiv& cdiv, int C, int cw,
-                                         int lane) {
+                                         float* gout, int np, const float2* taff, int cw, int lane) {
   switch (f.epi) {
-    case 0: seq_fast_paths<LAST, 0>(f, rg, in_s, out_s, gout, np, pb, cdiv, C, cw, lane); break;
-    case 1: seq_fast_paths<LAST, 1>(f, rg, in_s, out_s, gout, np, pb, cdiv, C, cw, lane); break;
-    case 2: seq_fast_paths<LAST, 2>(f, rg, in_s, out_s, gout, np, pb, cdiv, C, cw, lane); break;
-    default: seq_fast_paths<LAST, 3>(f, rg, in_s, out_s, gout, np, pb, cdiv, C, cw, lane); break;
+    case 0: seq_fast_paths<LAST, 0>(f, rg, in_s, out_s, gout, np, taff, cw, lane); break;
+    case 1: seq_fast_paths<LAST, 1>(f, rg, in_s, out_s, gout, np, taff, cw, lane); break;
+    case 2: seq_fast_paths<LAST, 2>(f, rg, in_s, out_s, gout, np, taff, cw, lane); break;
+    default: seq_fast_paths<LAST, 3>(f, rg, in_s, out_s, gout, np, taff, cw, lane); break;
   }
 }
 
@@ -186,8 +203,11 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
   uint64_t* full = (uint64_t*)smem;
   uint64_t* empty = full + 8;
   unsigned char* stage0 = smem + 128;
-  // the two ping-pong work buffers (selected by arithmetic, not a local array: no local memory)
-  float* const work0 = (float*)(stage0 + (size_t)a.stages * a.stage_bytes);
+  // steps ping-pong between the tile's stage and one work buffer: step k reads the stage (k even)
+  // or the work buffer (k odd) and writes the other, so a tile needs its stage + 1 buffer
+  float* const work = (float*)(stage0 + (size_t)a.stages * a.stage_bytes);
+  SeqRange* const t_rg = (SeqRange*)(work + (size_t)a.work_floats);               // [n_steps]
+  float2* const t_aff = (float2*)(t_rg + a.n_steps);                               // [n_steps][P]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_tiles = a.n_tiles;
   const int HW0 = a.in_plane;
@@ -262,22 +282,39 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
     const SeqRange* rgs = a.ranges + (size_t)band * a.n_steps;
     const int64_t pl0 = pg * a.tile_planes;
     const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
-    const float* src_base = (const float*)((const char*)stage0 + (size_t)s * a.stage_bytes +
-                                           ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW0 +
-                                                        (int64_t)rgs[0].in_lo * W_in) & 15u));
     const uint32_t pbase = (uint32_t)(a.plane0 + pl0);
+    // tile prologue: every step's row ranges and (scale, shift) per plane into shared memory, all
+    // loads in flight at once (the previous tile's last step ended with a CTA barrier)
+    {
+      const int tid = threadIdx.x - 32;
+      for (int i = tid; i < a.n_steps; i += 32 * kSeqWarps) t_rg[i] = rgs[i];
+      for (int i = tid; i < a.n_steps * np; i += 32 * kSeqWarps) {
+        const int st = i / np, p = i - st * np;
+        const float2* aff = tab[st].aff;
+        if (aff) {
+          const uint32_t plane = pbase + (uint32_t)p;
+          t_aff[st * a.tile_planes + p] = __ldg(aff + (plane - fdiv(plane, a.cdiv) * (uint32_t)a.C));
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kSeqWarps) : "memory");
+    }
+    float* const stage = (float*)((char*)stage0 + (size_t)s * a.stage_bytes);
+    const float* src_base = (const float*)((const char*)stage +
+                                           ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW0 +
+                                                        (int64_t)t_rg[0].in_lo * W_in) & 15u));
     for (int st_i = 0; st_i < a.n_steps; ++st_i) {
       const SeqStepSm& f = tab[st_i];
-      const SeqRange rg = rgs[st_i];
+      const SeqRange rg = t_rg[st_i];
       const bool last = st_i == a.n_steps - 1;
-      const float* in_buf = st_i == 0 ? src_base : work0 + ((st_i - 1) & 1) * a.work_floats;
-      float* out_buf = work0 + (st_i & 1) * a.work_floats;
+      const float* in_buf = st_i == 0 ? src_base : (st_i & 1) ? work : stage;
+      float* out_buf = (st_i & 1) ? stage : work;
       const int64_t HWo = (int64_t)f.Ho * f.Wo;
       float* gout = a.out + (a.plane0 + pl0) * HWo;
       if (f.path) {
         const uint32_t in_s = smem_u32(in_buf), out_s = smem_u32(out_buf);
-        if (last) seq_fast<true>(f, rg, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
-        else seq_fast<false>(f, rg, in_s, out_s, gout, np, pbase, a.cdiv, a.C, cw, lane);
+        const float2* taff = t_aff + st_i * a.tile_planes;
+        if (last) seq_fast<true>(f, rg, in_s, out_s, gout, np, taff, cw, lane);
+        else seq_fast<false>(f, rg, in_s, out_s, gout, np, taff, cw, lane);
       } else {
         const SeqStepDev& st = a.steps[st_i];
         // work items: (plane, output row, 32-column chunk); lane = output column
@@ -302,22 +339,230 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
         }
       }
       asm volatile("bar.sync 1, %0;" ::"r"(32 * kSeqWarps) : "memory");   // step boundary
-      if (st_i == 0 && cw == 0 && lane == 0) mbar_arrive(&empty[s]);      // stage buffer consumed
     }
+    if (cw == 0 && lane == 0) mbar_arrive(&empty[s]);   // the tile's stage is free for the producer
   }
+}
+
+// ------------------------------------------------------------------ in-place, warp per plane
+//
+// Sequences made only of fast steps (the §5.1 block) on whole planes of W <= 128: one or a few
+// consumer warps own a plane of the tile for the WHOLE sequence, so steps need no CTA barrier and
+// no work buffer.  The plane's rows are cut into parts, one per half-warp (16-lane segments, W <= 64)
+// or warp; parts of one plane in different warps meet at a named barrier twice per step (after each
+// part has read its neighbours' boundary rows, and at the end).  A step runs down a part's rows in place: output row i is written over input row i after
+// input row i+1 has been loaded, and the rows above are only needed as horizontal maxima already
+// held in registers; a lane loads and stores only its own 4 columns (neighbour columns arrive by
+// shuffle from the same load), so nothing is overwritten before it is read.  The one exception is
+// the row just below a part, which the next part overwrites first: it is read once, before any
+// part writes.  The next input row is loaded one
+// iteration ahead.  Shared memory per tile is the stage alone, so many CTAs share an SM and the bulk
+// copy of one CTA's next tile overlaps the other CTAs' steps.
+// One in-place step of one row part [r0, r0 + Hp) of a plane (Hp rows per part; the last part may
+// have fewer).  bar_id > 0: the plane's parts live in several warps (named barrier over them).
+template <int SEG, bool LAST, int EPI>
+__device__ __forceinline__ void inplace_step(uint32_t pbase, float* og, int H, int W, int c, bool st_ok, float2 aff,
+                                             int r0, int Hp, int bar_id, int bar_threads) {
+  const uint32_t W4 = 4u * (uint32_t)W;
+  auto hraw = [&](const float4& x) -> float4 {
+    float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
+    float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
+    l = c == 0 ? x.x : l;
+    rr = c + 4 >= W ? x.w : rr;
+    return make_float4(max3f(l, x.x, x.y), max3f(x.x, x.y, x.z), max3f(x.y, x.z, x.w), max3f(x.z, x.w, rr));
+  };
+  auto epi = [&](float v) -> float {
+    if (EPI >= 2) v = __fmaf_rn(v, aff.x, aff.y);
+    if (EPI == 1 || EPI == 3) v = relu(v);
+    return v;
+  };
+  const int rows = max(0, min(H, r0 + Hp) - r0);       // rows this part outputs
+  const uint32_t bottom = pbase + (uint32_t)(H - 1) * W4;
+  auto rad = [&](int r) -> uint32_t { return pbase + (uint32_t)min(max(r, 0), H - 1) * W4; };   // clamped
+  // everything this part reads from outside its own rows, before any part writes
+  const float4 x_bound = lds128(rad(r0 + Hp));         // the row below the part (or the bottom row)
+  float4 hA = hraw(lds128(rad(r0 - 1)));               // the row above (a duplicate at the top edge)
+  float4 hB = hraw(lds128(rad(r0)));
+  float4 x1 = lds128(rad(r0 + 1));                     // raw row r0 + 1, one ahead
+  if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+  uint32_t ad = rad(r0);
+  float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
+  float4 hC;
+  // main rows: rows i + 1 and i + 2 are the part's own (not yet overwritten)
+  auto row = [&](int i, const float4& a, const float4& b, float4& nx) {
+    const float4 x2 = lds128(min(ad + 2u * W4, bottom));   // raw row i + 2, before row i is overwritten
+    nx = hraw(x1);                                         // row i + 1
+    x1 = x2;
+    float4 o;
+    o.x = epi(max3f(a.x, b.x, nx.x));
+    o.y = epi(max3f(a.y, b.y, nx.y));
+    o.z = epi(max3f(a.z, b.z, nx.z));
+    o.w = epi(max3f(a.w, b.w, nx.w));
+    if (st_ok && i < rows) {
+      if (LAST) st_stream4(o_g, o);
+      else sts128(ad, o);
+    }
+    if (LAST) o_g += W;
+    ad += W4;
+  };
+  int i = 0;
+  for (; i + 5 <= Hp; i += 3) {
+    row(i, hA, hB, hC);
+    row(i + 1, hB, hC, hA);
+    row(i + 2, hC, hA, hB);
+  }
+  // the last rows: row i + 1 / i + 2 may lie below the part -> the row saved before the step
+  for (; i < Hp; ++i) {
+    const float4 x2 = i + 2 < Hp ? lds128(min(ad + 2u * W4, bottom)) : x_bound;
+    hC = hraw(i + 1 < Hp ? x1 : x_bound);
+    x1 = x2;
+    float4 o;
+    o.x = epi(max3f(hA.x, hB.x, hC.x));
+    o.y = epi(max3f(hA.y, hB.y, hC.y));
+    o.z = epi(max3f(hA.z, hB.z, hC.z));
+    o.w = epi(max3f(hA.w, hB.w, hC.w));
+    if (st_ok && i < rows) {
+      if (LAST) st_stream4(o_g, o);
+      else sts128(ad, o);
+    }
+    if (LAST) o_g += W;
+    ad += W4;
+    hA = hB;
+    hB = hC;
+  }
+  if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+}
+
+template <int SEG, bool LAST>
+__device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, float* og, int H, int W, int c, bool st_ok,
+                                                 float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
+  switch (epi) {
+    case 0: inplace_step<SEG, LAST, 0>(base, og, H, W, c, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+    case 1: inplace_step<SEG, LAST, 1>(base, og, H, W, c, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+    case 2: inplace_step<SEG, LAST, 2>(base, og, H, W, c, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+    default: inplace_step<SEG, LAST, 3>(base, og, H, W, c, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+  }
+}
+
+template <int SEG>
+__global__ void __launch_bounds__(32 * (kInplaceWarps + 1)) seq_inplace(SeqArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int8_t epi_tab[kMaxSeqSteps];
+  __shared__ const float2* aff_tab[kMaxSeqSteps];
+  uint64_t* full = (uint64_t*)smem;
+  uint64_t* empty = full + 8;
+  unsigned char* stage0 = smem + 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_tiles = a.n_tiles;
+  const int H = a.steps[0].H, W = a.steps[0].W, HW = a.in_plane;
+  const int n = a.n_steps;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 32 * kInplaceWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const SeqStepDev& st = a.steps[i];
+    const bool aff = st.epi_class == PC_AFFINE || st.epi_class == PC_AFFINE_RELU;
+    const bool rl = st.epi_class == PC_RELU || st.epi_class == PC_AFFINE_RELU;
+    epi_tab[i] = (int8_t)((aff ? 2 : 0) + (rl ? 1 : 0));
+    aff_tab[i] = aff ? st.epi.affine[0] : nullptr;
+  }
+  __syncthreads();
+  pdl_wait();                   // previous kernel on the stream complete + visible
+  pdl_launch_dependents();
+
+  if (warp == 0) {  // producer: one elected lane bulk-copies each tile's planes
+    if (lane == 0) {
+      int k = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+        const int s = k % a.stages;
+        if (k >= a.stages) mbar_wait_sleep(&empty[s], ((k / a.stages) - 1) & 1);
+        const int64_t pl0 = t * a.tile_planes;
+        const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
+        const float* src = a.in + (a.plane0 + pl0) * (int64_t)HW;
+        const uint32_t head_off = (uint32_t)((uintptr_t)src & 15u);
+        float* dst = (float*)((char*)stage0 + (size_t)s * a.stage_bytes + head_off);
+        const uint32_t nbytes = (uint32_t)np * (uint32_t)HW * 4u;
+        const uint32_t h = min(nbytes, (16u - head_off) & 15u);
+        const uint32_t body = (nbytes - h) & ~15u;
+        for (uint32_t e = 0; e < h / 4; ++e) cp_async4(dst + e, src + e);
+        for (uint32_t e = (h + body) / 4; e < nbytes / 4; ++e) cp_async4(dst + e, src + e);
+        cp_async_mbar_arrive(&full[s]);
+        if (body) {
+          mbar_arrive_expect_tx(&full[s], body);
+          for (uint32_t off = 0; off < body; off += kBulkChunk)
+            bulk_g2s((char*)dst + h + off, (const char*)src + h + off, min(kBulkChunk, body - off), &full[s]);
+        } else {
+          mbar_arrive(&full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // warps_per_plane (= kInplaceWarps / tile_planes) consumer warps share a plane; its rows are cut
+  // into warps_per_plane * 32/SEG parts, one per half-warp (16-lane segments) or warp
+  const int cw = warp - 1;
+  const int wpp = kInplaceWarps / a.tile_planes;
+  const int sl = lane & (SEG - 1), half = lane / SEG;
+  const int c = 4 * sl;
+  const int part = (cw % wpp) * (32 / SEG) + half;
+  const int n_parts = wpp * (32 / SEG);
+  const int Hp = (H + n_parts - 1) / n_parts;
+  const int bar_id = wpp > 1 ? 1 + cw / wpp : 0;       // named barrier of the plane's warps
+  float2* const t_aff = (float2*)(stage0 + (size_t)a.stages * a.stage_bytes) + (size_t)cw * n;   // this warp's
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+    const int s = k % a.stages;
+    const int64_t pl0 = t * a.tile_planes;
+    const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
+    const int p = cw / wpp;                             // this warp's plane in the tile
+    const uint32_t plane = (uint32_t)(a.plane0 + pl0 + min(p, np - 1));
+    // (scale, shift) of this warp's plane for every step, all loads in flight at once
+    const uint32_t ch = plane - fdiv(plane, a.cdiv) * (uint32_t)a.C;
+    for (int i = lane; i < n; i += 32) t_aff[i] = aff_tab[i] ? __ldg(aff_tab[i] + ch) : make_float2(1.f, 0.f);
+    __syncwarp();
+    mbar_wait_sleep(&full[s], (k / a.stages) & 1);
+    const bool st_ok = p < np && c < W;
+    const char* sbase = (const char*)stage0 + (size_t)s * a.stage_bytes +
+                        ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW) & 15u);
+    const uint32_t base = smem_u32(sbase) + 4u * (uint32_t)(min(p, np - 1) * HW + c);
+    float* og = a.out + (int64_t)plane * HW + c;
+    for (int st = 0; st < n; ++st) {
+      const float2 aff = t_aff[st];
+      if (st == n - 1) inplace_step_epi<SEG, true>(epi_tab[st], base, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
+      else inplace_step_epi<SEG, false>(epi_tab[st], base, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
+    }
+    mbar_arrive(&empty[s]);   // every lane: the tile's stage is free for the producer
+  }
+}
+
+size_t seq_inplace_smem(const SeqArgs& a) {
+  return 128 + (size_t)a.stages * a.stage_bytes + (size_t)kInplaceWarps * a.n_steps * 8 + 1024;
+}
+
+static const void* seq_fn(const SeqArgs& a) {
+  if (a.inplace_seg == 16) return (const void*)seq_inplace<16>;
+  if (a.inplace_seg == 32) return (const void*)seq_inplace<32>;
+  return (const void*)seq_staged;
 }
 
 cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st) {
   void* args[] = {(void*)&a};
-  const size_t smem = seq_smem(a);
-  return launch_pdl((void*)seq_staged, dim3(grid), dim3(kSeqThreads), args, smem, st);
+  if (a.inplace_seg)
+    return launch_pdl(seq_fn(a), dim3(grid), dim3(32 * (kInplaceWarps + 1)), args, seq_inplace_smem(a), st);
+  return launch_pdl((void*)seq_staged, dim3(grid), dim3(kSeqThreads), args, seq_smem(a), st);
 }
 
 int seq_max_blocks_per_sm(const SeqArgs& a) {
-  const size_t smem = seq_smem(a);
+  const size_t smem = a.inplace_seg ? seq_inplace_smem(a) : seq_smem(a);
+  const int threads = a.inplace_seg ? 32 * (kInplaceWarps + 1) : kSeqThreads;
   int n = 0;
-  if (smem_kernel_setup((const void*)seq_staged) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, (void*)seq_staged, kSeqThreads, smem) != cudaSuccess) n = 0;
+  if (smem_kernel_setup(seq_fn(a)) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, seq_fn(a), threads, smem) != cudaSuccess) n = 0;
   return n;
 }
 

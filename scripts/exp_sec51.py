@@ -22,6 +22,7 @@ out_path = argv[0] if argv and argv[0] != "-" else None
 N, C, H = (int(argv[1]), int(argv[2]), int(argv[3])) if len(argv) >= 4 else (128, 64, 56)
 DEPTHS = [int(v) for v in argv[4].split(",")] if len(argv) >= 5 else [1, 2, 4, 8, 12, 16, 17, 20, 24, 32, 40]
 EAGER = "--no-eager" not in sys.argv
+EXTRA = json.loads(os.environ.get("BS_SEC51_OPTS", "{}"))   # extra plan options (dev sweeps)
 dev = torch.device("cuda")
 l2 = torch.cuda.get_device_properties(dev).L2_cache_size
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -57,7 +58,7 @@ for depth in DEPTHS:
     ys = [torch.empty(case.shape, device=dev) for _ in range(nset)]
     res = {"depth": depth, "shape": list(case.shape), "alg_bytes": nbytes}
     for policy, name in ((1, "1_step"), (5, "max_5_steps"), (-1, "unrestricted"), (0, "planner")):
-        plan = bs.bs_plan_create(case.layers, case.shape, {"max_steps_per_sequence": policy})
+        plan = bs.bs_plan_create(case.layers, case.shape, {"max_steps_per_sequence": policy, **EXTRA})
         info = bs.bs_plan_query(plan)
         ms = time_graph(lambda q: bs.bs_execute(plan, xs[q], ys[q]), nset)
         li = bs.bs_plan_query_launch(plan, 0)

@@ -112,8 +112,10 @@ def _sec51_split_depth(W, H, budget=110 * 1024, lanes=256):
     """Independent closed form of the paper's packing rule for §5.1 blocks on H x W
     planes with halo tiles: base tile = ceil(256 / W) output rows (one output per consumer lane),
     each 3x3/s1/p1 block adds one input row above and below; the sequence footprint is two ring
-    stages of step 0's input band + two work buffers of the largest intermediate band (fp32)
-    + 128 B of barriers + 1 KB slack.  Returns the most blocks one sequence holds."""
+    stages of step 0's input band (each also holds the odd steps' intermediates, which are
+    smaller) + one work buffer of the largest even-step intermediate band (fp32)
+    + 128 B of barriers + the per-tile table (40 B of row ranges and 8 B of BN scale/shift per
+    step, 128-B rounded) + 1 KB slack.  Returns the most blocks one sequence holds."""
     r0 = -(-lanes // W)
     d = 1
     while True:
@@ -122,7 +124,8 @@ def _sec51_split_depth(W, H, budget=110 * 1024, lanes=256):
         rows_mid = min(H, r0 + 2 * (n - 1))          # the largest intermediate (step 0's output)
         stage = -(-(rows_in * W * 4 + 16) // 128) * 128
         work = -(-(rows_mid * W) // 4) * 4 * 4
-        if 128 + 2 * stage + 2 * work + 1024 > budget:
+        table = -(-(n * 40 + n * 8) // 128) * 128
+        if 128 + 2 * stage + work + table + 1024 > budget:
             return d
         d = n
 
@@ -138,7 +141,7 @@ def test_halo_sequence_split_depth(bs, H, depth):
     p = host_plan(bs, layers, (2, 4, H, H), max_steps_per_sequence=-1)
     info = bs.bs_plan_query(p)
     d = _sec51_split_depth(H, H)
-    whole = 128 + 2 * (-(-(H * H * 4 + 16) // 128) * 128) + 2 * H * H * 4 + 1024 <= 220 * 1024
+    whole = 128 + 2 * (-(-(H * H * 4 + 16) // 128) * 128) + H * H * 4 + 1024 <= 220 * 1024
     if whole:
         assert info["n_sequences"] == -(-depth // 64)
         return
@@ -317,9 +320,10 @@ def test_smem_budget_option(bs):
     drop to fewer stages or to the global-memory walker (the paper's cache budget)."""
     sec = synth.synthetic51(4, batch=2, C=3, H=56)
     assert bs.bs_plan_query(host_plan(bs, sec.layers, sec.shape))["n_launches"] == 1
-    # 40 KB: whole 56x56 planes no longer fit -> halo tiles, split where the closed form says
-    small = bs.bs_plan_create(sec.layers, sec.shape, {"host_only": 1, "smem_budget_bytes": 40 * 1024})
-    d = _sec51_split_depth(56, 56, budget=40 * 1024)
+    # 20 KB: whole 56x56 planes no longer fit (in-place: 2 planes = 25 KB; staged: 3 buffers)
+    # -> halo tiles, split where the closed form says
+    small = bs.bs_plan_create(sec.layers, sec.shape, {"host_only": 1, "smem_budget_bytes": 20 * 1024})
+    d = _sec51_split_depth(56, 56, budget=20 * 1024)
     assert bs.bs_plan_query(small)["n_launches"] == -(-4 // d)
     assert bs.bs_plan_query_launch(small, 0)["tile_rows"] > 0
     tiny = bs.bs_plan_create(sec.layers, sec.shape, {"host_only": 1, "smem_budget_bytes": 4 * 1024})

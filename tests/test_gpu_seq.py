@@ -116,3 +116,24 @@ def test_sec51_full_shapes_sampled(shape, depth, cuda_dev, oracle_lib):
     for n in (0, shape[0] - 1):
         ref = oracle.run_bf(case.layers, x[n:n + 1].cpu().numpy())
         U.check(out[n:n + 1].cpu().numpy(), ref, case.layers, f"{shape} image {n}")
+
+
+@pytest.mark.parametrize("H", [1, 2, 3, 4, 5, 7, 23, 56])
+def test_inplace_kernel_heights(H, cuda_dev, oracle_lib):
+    """The warp-per-plane in-place kernel (whole planes, W <= 128): odd/even heights (the two
+    half-warps split the rows), a partial last tile (odd plane count), every epilogue class; bit
+    for bit equal to the shared-tile kernel (force_tile_planes routes there) and to the oracle."""
+    bs = _bs()
+    for W in (4, 16, 56, 64, 68, 128):
+        shape = (1, 3, H, W)
+        layers = [synth.maxpool(3, 1, 1), synth.batchnorm(3, 1, signed_gamma=True), synth.relu(),
+                  synth.maxpool(3, 1, 1), synth.relu(), synth.maxpool(3, 1, 1), synth.batchnorm(3, 2),
+                  synth.maxpool(3, 1, 1)]
+        x = synth.uniform_np(H * 1000 + W, int(np.prod(shape))).reshape(shape)
+        got, plan = run_gpu(layers, x)
+        li = bs.bs_plan_query_launch(plan, 0)
+        assert li["kernel_name"] == "sequence_staged_tma" and li["block"] == 160, li   # in-place kernel
+        U.assert_close(got, oracle.run_bf(layers, x), f"H={H} W={W}")
+        other, plan2 = run_gpu(layers, x, {"force_tile_planes": 1})
+        assert bs.bs_plan_query_launch(plan2, 0)["block"] != 160
+        U.assert_bitexact(got, other, f"H={H} W={W} in-place vs shared tile")
