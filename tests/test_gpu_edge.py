@@ -133,13 +133,14 @@ def test_input_variants_every_baseline_stack(variant, cuda_dev, oracle_lib):
 @pytest.mark.parametrize("variant", ["allneg", "ties", "signed_zero"])
 def test_input_variants_every_kernel_family(variant, cuda_dev, oracle_lib):
     """The variants through each pool kernel family (forced), with a signed-gamma BN prologue."""
-    shape = (2, 4, 27, 28)
+    shape = (2, 4, 28, 28)
     n = int(np.prod(shape))
     x = synth.variant_np(variant, 5, n).reshape(shape)
     stacks = [[synth.relu(), synth.maxpool(3, 2)], [synth.maxpool(3, 2, 1)],
               [synth.batchnorm(4, 9, signed_gamma=True), synth.relu(), synth.maxpool(3, 2, 1)],
               [synth.batchnorm(4, 9, signed_gamma=True), synth.maxpool(2, 2)],
-              [synth.relu(), synth.avgpool(3, 2, 1)]]
+              [synth.batchnorm(4, 9, signed_gamma=True), synth.relu(), synth.avgpool(2, 2)],
+              [synth.relu(), synth.avgpool(3, 2, 1)], [synth.batchnorm(4, 3), synth.relu(), synth.avgpool(7, 7)]]
     for layers in stacks:
         ref = oracle.run_bf(layers, x)
         for g in (0, 1, 2, 3):
