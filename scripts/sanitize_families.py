@@ -43,6 +43,11 @@ FAMILIES = [
      "pool_staged_tma"),
     ("seq_fast", synth.synthetic51(4, batch=64, C=C, H=20).layers, (64, C, 20, 20), {"force_tile_planes": 1},
      "sequence_staged_tma"),
+    ("seq_inplace", synth.synthetic51(4, batch=64, C=C, H=20).layers, (64, C, 20, 20), None, "sequence_staged_tma"),
+    ("seq_inplace_wide", synth.synthetic51(3, batch=8, C=C, H=100).layers, (8, C, 100, 100), None,
+     "sequence_staged_tma"),
+    ("seq_halo", synth.synthetic51(5, batch=2, C=C, H=64).layers, (2, C, 64, 64), {"force_rows_per_task": 7},
+     "sequence_staged_tma"),
     ("seq_generic", [synth.maxpool(3, 1, 1), synth.relu(), synth.avgpool(2, 2), synth.batchnorm(C, 8),
                      synth.maxpool(3, 2, 1)], (64, C, 24, 22), {"force_tile_planes": 1}, "sequence_staged_tma"),
 ]
