@@ -354,6 +354,7 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
       if (cost < best * (1 - 1e-9)) { best = cost; bP = m * G; bR = R; }
     }
   }
+  const bool read_dominated = 8 * st.out.h * st.out.w < HW;   // global averages
   const int64_t stride = (int64_t)pool_staged_stride((int)bP, (int)HW);
   if (stride > 100 * 1024) return false;   // plane group too large to stage
   l.tile_planes = (int32_t)bP;
@@ -366,13 +367,13 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
   // 1 x 7 stages 6.5 us; DenseNet final, 31 KB tiles, 11 per SM: 2 CTAs).
   // (read-dominated pools -- global averages, output < 1/8 of the input -- gain from twice that:
   // DenseNet-121 final 7x7 average, 2 x 3 x 31 KB: 10.7 us vs 11.6 us at 2 x 2)
-  const int64_t kInflightPerSm = 8 * st.out.h * st.out.w < HW ? 208 * 1024 : 104 * 1024;
+  const int64_t kInflightPerSm = read_dominated ? 208 * 1024 : 104 * 1024;
   const int64_t tiles_per_sm = (n_planes + bP - 1) / bP / std::max(1, num_sms);
   // one CTA per SM only for big tiles, long kernels and pools that shrink the plane (stride >= 2:
   // few outputs per staged byte); stride-1 pools (the §5.1 block: one output per input) need the
   // second CTA's consumer warps (41 vs 47 us per block measured)
   const bool shrinks = 2 * st.out.h * st.out.w <= HW;
-  l.ctas_per_sm = (stride >= 20 * 1024 && tiles_per_sm >= 12 && shrinks) ? 1 : 2;
+  l.ctas_per_sm = (stride >= 20 * 1024 && tiles_per_sm >= 12 && shrinks && !read_dominated) ? 1 : 2;
   l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kStagedMaxStages,
                                                             (kInflightPerSm / l.ctas_per_sm + stride / 2) / stride));
   if (o.force_stages >= 2) l.stages = std::min(kStagedMaxStages, o.force_stages);

@@ -89,6 +89,16 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
 }
+// Predicated LDS.128: lanes past the row end (idle columns) load nothing (they would read other
+// threads' rows or tables; their values only feed outputs that are never stored or replaced).
+__device__ __forceinline__ float4 lds128_if(bool p, uint32_t a) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %4, 0;\n@q ld.shared.v4.f32 {%0,%1,%2,%3}, [%5];\n}\n"
+      : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+      : "r"((uint32_t)p), "r"(a));
+  return v;
+}
 __device__ __forceinline__ void sts128(uint32_t a, const float4& v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
@@ -121,7 +131,7 @@ __device__ __forceinline__ void seq_fast_step(const SeqStepSm& f, const SeqRange
     const uint32_t rowbase = in_s + 4u * (uint32_t)(p * f.in_pitch + c);
     // horizontal 3-max of the row at shared address ad (4 columns of this lane)
     auto hrow = [&](uint32_t ad) -> float4 {
-      const float4 x = lds128(ad);
+      const float4 x = lds128_if(col_ok, ad);
       float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
       float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
       if (NSEG > 1) {   // neighbours across segment boundaries come from shared memory
@@ -376,6 +386,8 @@ __device__ __forceinline__ void inplace_step(uint32_t pbase, float* og, int H, i
     if (EPI == 1 || EPI == 3) v = relu(v);
     return v;
   };
+  const bool col_ok = c < W;
+  auto lds128 = [&](uint32_t a) { return lds128_if(col_ok, a); };
   const int rows = max(0, min(H, r0 + Hp) - r0);       // rows this part outputs
   const uint32_t bottom = pbase + (uint32_t)(H - 1) * W4;
   auto rad = [&](int r) -> uint32_t { return pbase + (uint32_t)min(max(r, 0), H - 1) * W4; };   // clamped
@@ -385,6 +397,7 @@ __device__ __forceinline__ void inplace_step(uint32_t pbase, float* og, int H, i
   float4 hB = hraw(lds128(rad(r0)));
   float4 x1 = lds128(rad(r0 + 1));                     // raw row r0 + 1, one ahead
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+  else __syncwarp();                                   // the other half-warp's part
   uint32_t ad = rad(r0);
   float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
   float4 hC;
@@ -431,6 +444,7 @@ __device__ __forceinline__ void inplace_step(uint32_t pbase, float* og, int H, i
     hB = hC;
   }
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+  else __syncwarp();
 }
 
 template <int SEG, bool LAST>

@@ -71,6 +71,10 @@ def main():
         torch.cuda.synchronize()
         U.check(out.cpu().numpy(), oracle.run_bf(layers, x, ops), layers, name)
         print(f"{name}: {kname} grid {li['grid']} block {li['block']} smem {li['smem_bytes']} OK", flush=True)
+        del xd, out
+        bs.bs_plan_destroy(plan)             # plan-owned device memory freed before exit (leak check)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()                 # torch's cached blocks too
     print("ALL OK")
 
 
