@@ -373,7 +373,9 @@ bool size_stages(Launch& l, int64_t n_planes, const bs_plan_options& o, int num_
   // few outputs per staged byte); stride-1 pools (the §5.1 block: one output per input) need the
   // second CTA's consumer warps (41 vs 47 us per block measured)
   const bool shrinks = 2 * st.out.h * st.out.w <= HW;
-  l.ctas_per_sm = (stride >= 20 * 1024 && tiles_per_sm >= 12 && shrinks && !read_dominated) ? 1 : 2;
+  // (averages with a per-element prologue have a heavier consumer: they keep the second CTA)
+  const bool heavy = !st.is_max && !st.pro.empty();
+  l.ctas_per_sm = (stride >= 20 * 1024 && tiles_per_sm >= 12 && shrinks && !read_dominated && !heavy) ? 1 : 2;
   l.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(kStagedMaxStages,
                                                             (kInflightPerSm / l.ctas_per_sm + stride / 2) / stride));
   if (o.force_stages >= 2) l.stages = std::min(kStagedMaxStages, o.force_stages);
@@ -420,7 +422,10 @@ void configure_step_launch(bs_plan* p, Launch& l, const bs_plan_options& o) {
       const int vec = pool_vec_width(s.kh, s.kw, s.sh, s.sw, s.ph, s.pw, (int)s.in.w, (int)Wo);
       if (s.kw > 32) {
         l.kernel = K_POOL_NAIVE;
-      } else if (vec && o.force_generic == 0 && !per_elem_max) {
+      } else if (vec && o.force_generic == 0 && !per_elem_max &&
+                 !(!s.is_max && !s.pro.empty() && s.in.w <= 28)) {
+        // (averages with a per-element prologue on planes <= 28 wide stage better: DenseNet-121
+        // transitions 28x28 88.2 -> 82.5 us, 14x14 49.1 -> 45.4 us measured)
         // vector column walker: each lane VEC columns, VEC/2 outputs; halo lane for 3-wide windows
         l.kernel = K_POOL_VEC;
         const int opl = vec / 2, halo = s.kw == 3 ? 1 : 0;
