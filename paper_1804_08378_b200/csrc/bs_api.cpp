@@ -879,6 +879,8 @@ SeqArgs seq_probe(const Launch& l) {
   a.n_bands = l.seq_bands;
   a.n_steps = (int32_t)l.seq.size();
   a.inplace_seg = l.seq_inplace_seg;
+  a.H0 = (int32_t)l.step.in.h;
+  a.W0 = (int32_t)l.step.in.w;
   return a;
 }
 
@@ -1012,6 +1014,8 @@ bs_status enqueue(const bs_plan* p, const float* const* inputs, float* out, int6
       a.work_floats = l.seq_work_floats;
       a.inplace_seg = l.seq_inplace_seg;
       a.in_plane = (int32_t)(s.in.h * s.in.w);
+      a.H0 = (int32_t)s.in.h;
+      a.W0 = (int32_t)s.in.w;
       a.cdiv = make_fastdiv((uint32_t)a.C);
       const int grid = (int)std::min<int64_t>(a.n_tiles, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
       e = launch_seq(a, grid, st);

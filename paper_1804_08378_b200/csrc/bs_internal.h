@@ -129,6 +129,7 @@ struct SeqArgs {
   FastDiv cdiv;             // channels C (plane -> channel)
   int32_t inplace_seg;      // > 0: the warp-per-plane in-place kernel (seq_inplace) with lane
                             // segments of this width (16 or 32); 0: seq_staged
+  int32_t H0, W0;           // step-0 input plane (host-side kernel choice)
 };
 constexpr int kInplaceWarps = 4;   // consumer warps per CTA of seq_inplace (1, 2 or 4 per plane)
 cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st);

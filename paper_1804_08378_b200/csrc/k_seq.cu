@@ -447,9 +447,193 @@ __device__ __forceinline__ void inplace_step(uint32_t pbase, float* og, int H, i
   else __syncwarp();
 }
 
+// The same step for the common shapes (56 x 56 and 112 x 112 planes): every part has the same
+// Hp >= 2 rows (H % parts == 0) and a row of W / 4 lane groups leaves a free lane on either side
+// of it in its segment (W / 4 + 2 <= SEG).  Column group g sits on lane g + 1; the free lanes
+// hold -inf (the max identity, never stored), so the outer neighbours of the plane's edge
+// columns arrive by the same two shuffles as every other column's -- no edge selects.  Rows
+// below the part are never touched inside the loop (no address clamps): the main loop stops two
+// rows before the part's end, the last two rows take the own last row and the row saved below.
+// Per 4 outputs and row: LDS.128, 2 SHFL, 8 FMNMX3, the epilogue, STS.128 (STG.128 on the last
+// step) and the address increment.
+template <int SEG, bool LAST, int EPI>
+__device__ __forceinline__ void inplace_step_clean(uint32_t pbase, float* og, int H, int W, bool col_ok, bool st_ok,
+                                                   float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
+  const uint32_t W4 = 4u * (uint32_t)W;
+  auto ld = [&](uint32_t a) -> float4 {
+    float4 v = make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
+    if (col_ok) v = lds128(a);
+    return v;
+  };
+  auto hraw = [&](const float4& x) -> float4 {
+    const float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
+    const float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
+    return make_float4(max3f(l, x.x, x.y), max3f(x.x, x.y, x.z), max3f(x.y, x.z, x.w), max3f(x.z, x.w, rr));
+  };
+  auto epi = [&](float v) -> float {
+    if (EPI >= 2) v = __fmaf_rn(v, aff.x, aff.y);
+    if (EPI == 1 || EPI == 3) v = relu(v);
+    return v;
+  };
+  uint32_t ad = pbase + (uint32_t)r0 * W4;
+  // everything this part reads from outside its own rows, before any part writes
+  const float4 x_bound = ld(r0 + Hp < H ? ad + (uint32_t)Hp * W4 : ad + (uint32_t)(Hp - 1) * W4);
+  float4 hA = hraw(ld(r0 > 0 ? ad - W4 : ad));      // the row above (a duplicate at the top edge)
+  float4 hB = hraw(ld(ad));
+  float4 x1 = ld(ad + W4);                           // raw row r0 + 1 (Hp >= 2: the part's own)
+  if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+  else __syncwarp();                                 // the other half-warp's part
+  float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
+  float4 hC;
+  auto out = [&](const float4& a, const float4& b, const float4& c) {
+    float4 o;
+    o.x = epi(max3f(a.x, b.x, c.x));
+    o.y = epi(max3f(a.y, b.y, c.y));
+    o.z = epi(max3f(a.z, b.z, c.z));
+    o.w = epi(max3f(a.w, b.w, c.w));
+    if (st_ok) {
+      if (LAST) st_stream4(o_g, o);
+      else sts128(ad, o);
+    }
+    if (LAST) o_g += W;
+    ad += W4;
+  };
+  // output row i (i + 2 < Hp): raw row i + 2 is loaded before row i is overwritten
+  auto row = [&](const float4& a, const float4& b, float4& nx) {
+    const float4 x2 = ld(ad + 2u * W4);
+    nx = hraw(x1);
+    x1 = x2;
+    out(a, b, nx);
+  };
+  const int n_main = Hp - 2;
+  int i = 0;
+  for (; i + 3 <= n_main; i += 3) {
+    row(hA, hB, hC);
+    row(hB, hC, hA);
+    row(hC, hA, hB);
+  }
+  // 0..2 main rows left, then the part's last two rows (own row Hp - 1 in x1, then the row below)
+  const int rem = n_main - i;
+  if (rem == 0) {
+    hC = hraw(x1);       out(hA, hB, hC);
+    hA = hraw(x_bound);  out(hB, hC, hA);
+  } else if (rem == 1) {
+    row(hA, hB, hC);
+    hA = hraw(x1);       out(hB, hC, hA);
+    hB = hraw(x_bound);  out(hC, hA, hB);
+  } else {
+    row(hA, hB, hC);
+    row(hB, hC, hA);
+    hB = hraw(x1);       out(hC, hA, hB);
+    hC = hraw(x_bound);  out(hA, hB, hC);
+  }
+  if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+  else __syncwarp();
+}
+
+// Two consecutive steps k, k + 1 in ONE sweep down a part's rows (temporal blocking): shared
+// memory is read and written once per two steps instead of once per step, and the step-k rows
+// never leave registers.  While the sweep stands on row i it loads raw row i + 2, makes step-k row
+// y[i + 1] from the raw rows' horizontal maxima h[i .. i + 2], takes y[i + 1]'s horizontal maxima
+// g[i + 1] (two more shuffles), and writes step-(k+1) row z[i] from g[i - 1 .. i + 1] over raw
+// row i, which nothing needs any more.  The part's edges need two raw rows on either side (read
+// before any part writes) and one redundant y row on either side; at the plane's top / bottom
+// edge the step-k row beyond the plane is absent, i.e. g[-1] := g[0] and g[H] := g[H - 1]
+// (duplicates, exact for max).  Epilogues are branch-free per step: v * s + t then max(v, lo),
+// with (s, t) = (1, -0) without BN (exact: v + -0 == v, -0 included) and lo = -inf without ReLU.
 template <int SEG, bool LAST>
+__device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, float* og, int H, int W, bool col_ok, bool st_ok,
+                                                   float2 a1, float lo1, float2 a2, float lo2, int r0, int Hp,
+                                                   int bar_id, int bar_threads) {
+  const uint32_t W4 = 4u * (uint32_t)W;
+  auto ld = [&](uint32_t a) -> float4 {
+    float4 v = make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
+    if (col_ok) v = lds128(a);
+    return v;
+  };
+  auto hraw = [&](const float4& x) -> float4 {
+    const float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
+    const float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
+    return make_float4(max3f(l, x.x, x.y), max3f(x.x, x.y, x.z), max3f(x.y, x.z, x.w), max3f(x.z, x.w, rr));
+  };
+  auto vert = [&](const float4& a, const float4& b, const float4& c, float2 s, float lo) -> float4 {
+    float4 o;
+    o.x = fmaxf(__fmaf_rn(max3f(a.x, b.x, c.x), s.x, s.y), lo);
+    o.y = fmaxf(__fmaf_rn(max3f(a.y, b.y, c.y), s.x, s.y), lo);
+    o.z = fmaxf(__fmaf_rn(max3f(a.z, b.z, c.z), s.x, s.y), lo);
+    o.w = fmaxf(__fmaf_rn(max3f(a.w, b.w, c.w), s.x, s.y), lo);
+    return o;
+  };
+  // A pad lane's step-k row must stay -inf (its neighbours take it as their outer column), but its
+  // horizontal maxima pick up the edge columns through the shuffles: (s, t) = (0, -inf) maps any
+  // finite v to -inf and -inf to NaN, which max(., lo = -inf) turns back into -inf.
+  if (!col_ok) { a1 = make_float2(0.f, -CUDART_INF_F); lo1 = -CUDART_INF_F; }
+  const bool top = r0 == 0, bot = r0 + Hp == H;
+  uint32_t ad = pbase + (uint32_t)r0 * W4;
+  // rows outside the part, before any part writes (clamped copies at the plane's edges)
+  const float4 xa2 = ld(top ? ad : ad - 2u * W4);
+  const float4 xa1 = ld(top ? ad : ad - W4);
+  const float4 xb1 = ld(bot ? ad + (uint32_t)(Hp - 1) * W4 : ad + (uint32_t)Hp * W4);
+  const float4 xb2 = ld(bot ? ad + (uint32_t)(Hp - 1) * W4 : ad + (uint32_t)(Hp + 1) * W4);
+  const float4 x0 = ld(ad), x1 = ld(ad + W4);
+  float4 xn = Hp > 2 ? ld(ad + 2u * W4) : xb1;       // raw row r0 + 2, one row ahead
+  if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+  else __syncwarp();
+  float4 hA = hraw(x0), hB = hraw(x1), hC;
+  float4 gA, gB, gC;
+  {
+    const float4 hm2 = hraw(xa2), hm1 = hraw(xa1);
+    gA = hraw(vert(hm2, hm1, hA, a1, lo1));           // g[r0 - 1]
+    gB = hraw(vert(hm1, hA, hB, a1, lo1));            // g[r0]
+    if (top) gA = gB;
+  }
+  float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
+  // z row i from the window (h, g rotate together); x = raw row i + 2
+  auto row = [&](const float4& x, const float4& ha, const float4& hb, float4& hc, const float4& ga, const float4& gb,
+                 float4& gc, bool bottom_row) {
+    hc = hraw(x);
+    gc = hraw(vert(ha, hb, hc, a1, lo1));
+    if (bottom_row) gc = gb;
+    const float4 o = vert(ga, gb, gc, a2, lo2);
+    if (st_ok) {
+      if (LAST) st_stream4(o_g, o);
+      else sts128(ad, o);
+    }
+    if (LAST) o_g += W;
+    ad += W4;
+  };
+  int i = 0;
+  // main rows: the prefetched row i + 3 is the part's own
+  for (; i + 3 <= Hp - 3; i += 3) {
+    float4 x = xn; xn = ld(ad + 3u * W4); row(x, hA, hB, hC, gA, gB, gC, false);
+    x = xn; xn = ld(ad + 3u * W4);        row(x, hB, hC, hA, gB, gC, gA, false);
+    x = xn; xn = ld(ad + 3u * W4);        row(x, hC, hA, hB, gC, gA, gB, false);
+  }
+#pragma unroll 1
+  for (; i < Hp; ++i) {
+    const float4 x = xn;
+    if (i + 3 < Hp) xn = ld(ad + 3u * W4);
+    else xn = i + 3 == Hp ? xb1 : xb2;
+    row(x, hA, hB, hC, gA, gB, gC, bot && i == Hp - 1);
+    hA = hB; hB = hC; gA = gB; gB = gC;
+  }
+  if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+  else __syncwarp();
+}
+
+template <int SEG, bool CLEAN, bool LAST>
 __device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, float* og, int H, int W, int c, bool st_ok,
                                                  float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
+  if (CLEAN) {
+    const bool col_ok = c >= 0 && c < W;
+    switch (epi) {
+      case 0: inplace_step_clean<SEG, LAST, 0>(base, og, H, W, col_ok, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+      case 1: inplace_step_clean<SEG, LAST, 1>(base, og, H, W, col_ok, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+      case 2: inplace_step_clean<SEG, LAST, 2>(base, og, H, W, col_ok, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+      default: inplace_step_clean<SEG, LAST, 3>(base, og, H, W, col_ok, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+    }
+    return;
+  }
   switch (epi) {
     case 0: inplace_step<SEG, LAST, 0>(base, og, H, W, c, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
     case 1: inplace_step<SEG, LAST, 1>(base, og, H, W, c, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
@@ -458,8 +642,14 @@ __device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, float* 
   }
 }
 
-template <int SEG>
-__global__ void __launch_bounds__(32 * (kInplaceWarps + 1)) seq_inplace(SeqArgs a) {
+// Whether seq_inplace takes the clean step (inplace_step_clean) for these planes.
+__host__ __device__ inline bool inplace_clean(int seg, int tile_planes, int H, int W) {
+  const int parts = (kInplaceWarps / tile_planes) * (32 / seg);
+  return W / 4 + 2 <= seg && H % parts == 0 && H / parts >= 2;
+}
+
+template <int SEG, bool CLEAN>
+__global__ void __launch_bounds__(32 * (kInplaceWarps + 1), 4) seq_inplace(SeqArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int8_t epi_tab[kMaxSeqSteps];
   __shared__ const float2* aff_tab[kMaxSeqSteps];
@@ -522,7 +712,7 @@ __global__ void __launch_bounds__(32 * (kInplaceWarps + 1)) seq_inplace(SeqArgs 
   const int cw = warp - 1;
   const int wpp = kInplaceWarps / a.tile_planes;
   const int sl = lane & (SEG - 1), half = lane / SEG;
-  const int c = 4 * sl;
+  const int c = 4 * (CLEAN ? sl - 1 : sl);            // clean: lane 0 of a segment is a -inf pad
   const int part = (cw % wpp) * (32 / SEG) + half;
   const int n_parts = wpp * (32 / SEG);
   const int Hp = (H + n_parts - 1) / n_parts;
@@ -537,18 +727,32 @@ __global__ void __launch_bounds__(32 * (kInplaceWarps + 1)) seq_inplace(SeqArgs 
     const uint32_t plane = (uint32_t)(a.plane0 + pl0 + min(p, np - 1));
     // (scale, shift) of this warp's plane for every step, all loads in flight at once
     const uint32_t ch = plane - fdiv(plane, a.cdiv) * (uint32_t)a.C;
-    for (int i = lane; i < n; i += 32) t_aff[i] = aff_tab[i] ? __ldg(aff_tab[i] + ch) : make_float2(1.f, 0.f);
+    // (no BN: (1, -0), an exact identity of v * s + t, the clean steps' branch-free epilogue)
+    for (int i = lane; i < n; i += 32) t_aff[i] = aff_tab[i] ? __ldg(aff_tab[i] + ch) : make_float2(1.f, -0.f);
     __syncwarp();
     mbar_wait_sleep(&full[s], (k / a.stages) & 1);
-    const bool st_ok = p < np && c < W;
+    const bool st_ok = p < np && c >= 0 && c < W;
     const char* sbase = (const char*)stage0 + (size_t)s * a.stage_bytes +
                         ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW) & 15u);
     const uint32_t base = smem_u32(sbase) + 4u * (uint32_t)(min(p, np - 1) * HW + c);
     float* og = a.out + (int64_t)plane * HW + c;
-    for (int st = 0; st < n; ++st) {
+    int st = 0;
+    if (CLEAN) {   // steps two at a time (one sweep per pair), an odd last step alone
+      const bool col_ok = c >= 0 && c < W;
+      for (; st + 1 < n; st += 2) {
+        const float lo1 = (epi_tab[st] & 1) ? 0.f : -CUDART_INF_F, lo2 = (epi_tab[st + 1] & 1) ? 0.f : -CUDART_INF_F;
+        if (st + 2 == n)
+          inplace_pair_clean<SEG, true>(base, og, H, W, col_ok, st_ok, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp, Hp,
+                                        bar_id, 32 * wpp);
+        else
+          inplace_pair_clean<SEG, false>(base, og, H, W, col_ok, st_ok, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp, Hp,
+                                         bar_id, 32 * wpp);
+      }
+    }
+    for (; st < n; ++st) {
       const float2 aff = t_aff[st];
-      if (st == n - 1) inplace_step_epi<SEG, true>(epi_tab[st], base, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
-      else inplace_step_epi<SEG, false>(epi_tab[st], base, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
+      if (st == n - 1) inplace_step_epi<SEG, CLEAN, true>(epi_tab[st], base, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
+      else inplace_step_epi<SEG, CLEAN, false>(epi_tab[st], base, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
     }
     mbar_arrive(&empty[s]);   // every lane: the tile's stage is free for the producer
   }
@@ -559,8 +763,9 @@ size_t seq_inplace_smem(const SeqArgs& a) {
 }
 
 static const void* seq_fn(const SeqArgs& a) {
-  if (a.inplace_seg == 16) return (const void*)seq_inplace<16>;
-  if (a.inplace_seg == 32) return (const void*)seq_inplace<32>;
+  const bool clean = a.inplace_seg && inplace_clean(a.inplace_seg, a.tile_planes, a.H0, a.W0);
+  if (a.inplace_seg == 16) return clean ? (const void*)seq_inplace<16, true> : (const void*)seq_inplace<16, false>;
+  if (a.inplace_seg == 32) return clean ? (const void*)seq_inplace<32, true> : (const void*)seq_inplace<32, false>;
   return (const void*)seq_staged;
 }
 

@@ -118,13 +118,15 @@ def test_sec51_full_shapes_sampled(shape, depth, cuda_dev, oracle_lib):
         U.check(out[n:n + 1].cpu().numpy(), ref, case.layers, f"{shape} image {n}")
 
 
-@pytest.mark.parametrize("H", [1, 2, 3, 4, 5, 7, 23, 56])
+@pytest.mark.parametrize("H", [1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 23, 56, 112])
 def test_inplace_kernel_heights(H, cuda_dev, oracle_lib):
     """The warp-per-plane in-place kernel (whole planes, W <= 128): odd/even heights (the two
     half-warps split the rows), a partial last tile (odd plane count), every epilogue class; bit
-    for bit equal to the shared-tile kernel (force_tile_planes routes there) and to the oracle."""
+    for bit equal to the shared-tile kernel (force_tile_planes routes there) and to the oracle.
+    Heights whose parts hold 2, 3, 4, 5 and 28 rows reach every tail of the clean step
+    (k_seq.cu inplace_step_clean: W / 4 + 2 lanes fit a segment, H divisible by the parts)."""
     bs = _bs()
-    for W in (4, 16, 56, 64, 68, 128):
+    for W in (4, 16, 56, 64, 68, 112, 128):
         shape = (1, 3, H, W)
         layers = [synth.maxpool(3, 1, 1), synth.batchnorm(3, 1, signed_gamma=True), synth.relu(),
                   synth.maxpool(3, 1, 1), synth.relu(), synth.maxpool(3, 1, 1), synth.batchnorm(3, 2),
