@@ -99,6 +99,13 @@ __device__ __forceinline__ float4 lds128_if(bool p, uint32_t a) {
       : "r"((uint32_t)p), "r"(a));
   return v;
 }
+// Clean steps: every lane keeps its natural row address; a pad lane's loads are redirected into a
+// 128-B block of -inf at the same offset mod 128 -- the same bank group, so a quarter-warp's
+// LDS.128 stays conflict-free -- by one LOP3: (a & msk) | orv, msk = ~0 / orv = 0 for real lanes.
+struct PadLd {
+  uint32_t msk, orv;
+  __device__ __forceinline__ float4 operator()(uint32_t a) const { return lds128((a & msk) | orv); }
+};
 __device__ __forceinline__ void sts128(uint32_t a, const float4& v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
@@ -449,22 +456,16 @@ __device__ __forceinline__ void inplace_step(uint32_t pbase, float* og, int H, i
 
 // The same step for the common shapes (56 x 56 and 112 x 112 planes): every part has the same
 // Hp >= 2 rows (H % parts == 0) and a row of W / 4 lane groups leaves a free lane on either side
-// of it in its segment (W / 4 + 2 <= SEG).  Column group g sits on lane g + 1; the free lanes
-// hold -inf (the max identity, never stored), so the outer neighbours of the plane's edge
-// columns arrive by the same two shuffles as every other column's -- no edge selects.  Rows
-// below the part are never touched inside the loop (no address clamps): the main loop stops two
-// rows before the part's end, the last two rows take the own last row and the row saved below.
-// Per 4 outputs and row: LDS.128, 2 SHFL, 8 FMNMX3, the epilogue, STS.128 (STG.128 on the last
-// step) and the address increment.
+// of it in its segment (W / 4 + 2 <= SEG).  Column group g sits on lane g + 1; the free (pad)
+// lanes read -inf (PadLd) and never store, so the outer neighbours of the plane's edge columns
+// arrive by the same two shuffles as every other column's -- no edge selects, no predicated loads.  Rows below the part are never
+// touched inside the loop (no address clamps): the main loop stops two rows before the part's
+// end, the last two rows take the own last row and the row saved below.  Per 4 outputs and row:
+// LDS.128, 2 SHFL, 8 FMNMX3, the epilogue, STS.128 (STG.128 on the last step), one address add.
 template <int SEG, bool LAST, int EPI>
-__device__ __forceinline__ void inplace_step_clean(uint32_t pbase, float* og, int H, int W, bool col_ok, bool st_ok,
+__device__ __forceinline__ void inplace_step_clean(uint32_t pbase, PadLd ld, float* og, int H, int W, bool st_ok,
                                                    float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
   const uint32_t W4 = 4u * (uint32_t)W;
-  auto ld = [&](uint32_t a) -> float4 {
-    float4 v = make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
-    if (col_ok) v = lds128(a);
-    return v;
-  };
   auto hraw = [&](const float4& x) -> float4 {
     const float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
     const float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
@@ -478,9 +479,9 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, float* og, in
   uint32_t ad = pbase + (uint32_t)r0 * W4;
   // everything this part reads from outside its own rows, before any part writes
   const float4 x_bound = ld(r0 + Hp < H ? ad + (uint32_t)Hp * W4 : ad + (uint32_t)(Hp - 1) * W4);
-  float4 hA = hraw(ld(r0 > 0 ? ad - W4 : ad));      // the row above (a duplicate at the top edge)
+  float4 hA = hraw(ld(r0 > 0 ? ad - W4 : ad));   // the row above (a duplicate at the top edge)
   float4 hB = hraw(ld(ad));
-  float4 x1 = ld(ad + W4);                           // raw row r0 + 1 (Hp >= 2: the part's own)
+  float4 x1 = ld(ad + W4);                        // raw row r0 + 1 (Hp >= 2: the part's own)
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();                                 // the other half-warp's part
   float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
@@ -533,24 +534,21 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, float* og, in
 
 // Two consecutive steps k, k + 1 in ONE sweep down a part's rows (temporal blocking): shared
 // memory is read and written once per two steps instead of once per step, and the step-k rows
-// never leave registers.  While the sweep stands on row i it loads raw row i + 2, makes step-k row
-// y[i + 1] from the raw rows' horizontal maxima h[i .. i + 2], takes y[i + 1]'s horizontal maxima
-// g[i + 1] (two more shuffles), and writes step-(k+1) row z[i] from g[i - 1 .. i + 1] over raw
-// row i, which nothing needs any more.  The part's edges need two raw rows on either side (read
-// before any part writes) and one redundant y row on either side; at the plane's top / bottom
-// edge the step-k row beyond the plane is absent, i.e. g[-1] := g[0] and g[H] := g[H - 1]
-// (duplicates, exact for max).  Epilogues are branch-free per step: v * s + t then max(v, lo),
-// with (s, t) = (1, -0) without BN (exact: v + -0 == v, -0 included) and lo = -inf without ReLU.
+// never leave registers.  While the sweep stands on row i it takes raw row i + 2 (loaded one row
+// ahead), makes step-k row y[i + 1] from the raw rows' horizontal maxima h[i .. i + 2], takes
+// y[i + 1]'s horizontal maxima g[i + 1] (two more shuffles), and writes step-(k+1) row z[i] from
+// g[i - 1 .. i + 1] over raw row i, which nothing needs any more.  The part's edges need two raw
+// rows on either side (read before any part writes) and one redundant y row on either side; at
+// the plane's top / bottom edge the step-k row beyond the plane is absent, i.e. g[-1] := g[0] and
+// g[H] := g[H - 1] (duplicates, exact for max).  Epilogues are branch-free per step: v * s + t
+// then max(v, lo), with (s, t) = (1, -0) without BN (exact: v + -0 == v, -0 included) and
+// lo = -inf without ReLU.  The window rotates through three register roles (no moves): the main
+// loop is unrolled by 3 and the part's last 2..5 rows are unrolled per remainder.
 template <int SEG, bool LAST>
-__device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, float* og, int H, int W, bool col_ok, bool st_ok,
-                                                   float2 a1, float lo1, float2 a2, float lo2, int r0, int Hp,
-                                                   int bar_id, int bar_threads) {
+__device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, PadLd ld, float* og, int H, int W, bool col_ok,
+                                                   bool st_ok, float2 a1, float lo1, float2 a2, float lo2, int r0,
+                                                   int Hp, int bar_id, int bar_threads) {
   const uint32_t W4 = 4u * (uint32_t)W;
-  auto ld = [&](uint32_t a) -> float4 {
-    float4 v = make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
-    if (col_ok) v = lds128(a);
-    return v;
-  };
   auto hraw = [&](const float4& x) -> float4 {
     const float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
     const float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
@@ -576,7 +574,7 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, float* og, in
   const float4 xb1 = ld(bot ? ad + (uint32_t)(Hp - 1) * W4 : ad + (uint32_t)Hp * W4);
   const float4 xb2 = ld(bot ? ad + (uint32_t)(Hp - 1) * W4 : ad + (uint32_t)(Hp + 1) * W4);
   const float4 x0 = ld(ad), x1 = ld(ad + W4);
-  float4 xn = Hp > 2 ? ld(ad + 2u * W4) : xb1;       // raw row r0 + 2, one row ahead
+  float4 xn = Hp > 2 ? ld(ad + 2u * W4) : xb1;   // raw row r0 + 2, one row ahead
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();
   float4 hA = hraw(x0), hB = hraw(x1), hC;
@@ -588,7 +586,7 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, float* og, in
     if (top) gA = gB;
   }
   float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
-  // z row i from the window (h, g rotate together); x = raw row i + 2
+  // z row i from the window; x = raw row i + 2
   auto row = [&](const float4& x, const float4& ha, const float4& hb, float4& hc, const float4& ga, const float4& gb,
                  float4& gc, bool bottom_row) {
     hc = hraw(x);
@@ -602,35 +600,55 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, float* og, in
     if (LAST) o_g += W;
     ad += W4;
   };
+  // rotation phases: P0 = (A, B, C), P1 = (B, C, A), P2 = (C, A, B)
+#define BS_ROW0(x, b) row(x, hA, hB, hC, gA, gB, gC, b)
+#define BS_ROW1(x, b) row(x, hB, hC, hA, gB, gC, gA, b)
+#define BS_ROW2(x, b) row(x, hC, hA, hB, gC, gA, gB, b)
   int i = 0;
   // main rows: the prefetched row i + 3 is the part's own
   for (; i + 3 <= Hp - 3; i += 3) {
-    float4 x = xn; xn = ld(ad + 3u * W4); row(x, hA, hB, hC, gA, gB, gC, false);
-    x = xn; xn = ld(ad + 3u * W4);        row(x, hB, hC, hA, gB, gC, gA, false);
-    x = xn; xn = ld(ad + 3u * W4);        row(x, hC, hA, hB, gC, gA, gB, false);
+    float4 x = xn; xn = ld(ad + 3u * W4); BS_ROW0(x, false);
+    x = xn; xn = ld(ad + 3u * W4);        BS_ROW1(x, false);
+    x = xn; xn = ld(ad + 3u * W4);        BS_ROW2(x, false);
   }
-#pragma unroll 1
-  for (; i < Hp; ++i) {
-    const float4 x = xn;
-    if (i + 3 < Hp) xn = ld(ad + 3u * W4);
-    else xn = i + 3 == Hp ? xb1 : xb2;
-    row(x, hA, hB, hC, gA, gB, gC, bot && i == Hp - 1);
-    hA = hB; hB = hC; gA = gB; gB = gC;
+  // r own-prefetch rows left (r = Hp - 3 - i in {-1 (Hp == 2), 0, 1, 2}), then the part's last
+  // three rows, which take own row Hp - 1 (prefetched), the row below, the row after it
+  const int r = Hp - 3 - i;
+  if (r < 0) {
+    BS_ROW0(xn, false);
+    BS_ROW1(xb2, bot);
+  } else if (r == 0) {
+    BS_ROW0(xn, false);
+    BS_ROW1(xb1, false);
+    BS_ROW2(xb2, bot);
+  } else if (r == 1) {
+    float4 x = xn; xn = ld(ad + 3u * W4); BS_ROW0(x, false);
+    BS_ROW1(xn, false);
+    BS_ROW2(xb1, false);
+    BS_ROW0(xb2, bot);
+  } else {
+    float4 x = xn; xn = ld(ad + 3u * W4); BS_ROW0(x, false);
+    x = xn; xn = ld(ad + 3u * W4);        BS_ROW1(x, false);
+    BS_ROW2(xn, false);
+    BS_ROW0(xb1, false);
+    BS_ROW1(xb2, bot);
   }
+#undef BS_ROW0
+#undef BS_ROW1
+#undef BS_ROW2
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();
 }
 
 template <int SEG, bool CLEAN, bool LAST>
-__device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, float* og, int H, int W, int c, bool st_ok,
-                                                 float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
+__device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, PadLd W4, float* og, int H, int W, int c,
+                                                 bool st_ok, float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
   if (CLEAN) {
-    const bool col_ok = c >= 0 && c < W;
     switch (epi) {
-      case 0: inplace_step_clean<SEG, LAST, 0>(base, og, H, W, col_ok, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
-      case 1: inplace_step_clean<SEG, LAST, 1>(base, og, H, W, col_ok, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
-      case 2: inplace_step_clean<SEG, LAST, 2>(base, og, H, W, col_ok, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
-      default: inplace_step_clean<SEG, LAST, 3>(base, og, H, W, col_ok, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+      case 0: inplace_step_clean<SEG, LAST, 0>(base, W4, og, H, W, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+      case 1: inplace_step_clean<SEG, LAST, 1>(base, W4, og, H, W, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+      case 2: inplace_step_clean<SEG, LAST, 2>(base, W4, og, H, W, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+      default: inplace_step_clean<SEG, LAST, 3>(base, W4, og, H, W, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
     }
     return;
   }
@@ -653,6 +671,7 @@ __global__ void __launch_bounds__(32 * (kInplaceWarps + 1), 4) seq_inplace(SeqAr
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int8_t epi_tab[kMaxSeqSteps];
   __shared__ const float2* aff_tab[kMaxSeqSteps];
+  __shared__ __align__(128) float4 s_ninf[8];          // the clean steps' pad lanes read this
   uint64_t* full = (uint64_t*)smem;
   uint64_t* empty = full + 8;
   unsigned char* stage0 = smem + 128;
@@ -667,6 +686,7 @@ __global__ void __launch_bounds__(32 * (kInplaceWarps + 1), 4) seq_inplace(SeqAr
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (threadIdx.x < 8) s_ninf[threadIdx.x] = make_float4(-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const SeqStepDev& st = a.steps[i];
     const bool aff = st.epi_class == PC_AFFINE || st.epi_class == PC_AFFINE_RELU;
@@ -734,25 +754,29 @@ __global__ void __launch_bounds__(32 * (kInplaceWarps + 1), 4) seq_inplace(SeqAr
     const bool st_ok = p < np && c >= 0 && c < W;
     const char* sbase = (const char*)stage0 + (size_t)s * a.stage_bytes +
                         ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW) & 15u);
+    // clean: pad lanes read the -inf float4 at every row (row pitch 0) and never store
+    const bool col_ok = c >= 0 && c < W;
     const uint32_t base = smem_u32(sbase) + 4u * (uint32_t)(min(p, np - 1) * HW + c);
+    const PadLd W4{col_ok ? ~0u : 127u, col_ok ? 0u : smem_u32(s_ninf)};
     float* og = a.out + (int64_t)plane * HW + c;
     int st = 0;
     if (CLEAN) {   // steps two at a time (one sweep per pair), an odd last step alone
-      const bool col_ok = c >= 0 && c < W;
       for (; st + 1 < n; st += 2) {
         const float lo1 = (epi_tab[st] & 1) ? 0.f : -CUDART_INF_F, lo2 = (epi_tab[st + 1] & 1) ? 0.f : -CUDART_INF_F;
         if (st + 2 == n)
-          inplace_pair_clean<SEG, true>(base, og, H, W, col_ok, st_ok, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp, Hp,
-                                        bar_id, 32 * wpp);
+          inplace_pair_clean<SEG, true>(base, W4, og, H, W, col_ok, st_ok, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp,
+                                        Hp, bar_id, 32 * wpp);
         else
-          inplace_pair_clean<SEG, false>(base, og, H, W, col_ok, st_ok, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp, Hp,
-                                         bar_id, 32 * wpp);
+          inplace_pair_clean<SEG, false>(base, W4, og, H, W, col_ok, st_ok, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp,
+                                         Hp, bar_id, 32 * wpp);
       }
     }
     for (; st < n; ++st) {
       const float2 aff = t_aff[st];
-      if (st == n - 1) inplace_step_epi<SEG, CLEAN, true>(epi_tab[st], base, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
-      else inplace_step_epi<SEG, CLEAN, false>(epi_tab[st], base, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
+      if (st == n - 1)
+        inplace_step_epi<SEG, CLEAN, true>(epi_tab[st], base, W4, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
+      else
+        inplace_step_epi<SEG, CLEAN, false>(epi_tab[st], base, W4, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
     }
     mbar_arrive(&empty[s]);   // every lane: the tile's stage is free for the producer
   }

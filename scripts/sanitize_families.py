@@ -27,7 +27,7 @@ FAMILIES = [
     ("ew", [synth.batchnorm(C, 1), synth.relu()], (3, C, 13, 13), None, "ew_stream"),
     ("ew_add", [synth.batchnorm(C, 2), synth.add(1), synth.relu()], (3, C, 7, 7), None, "ew_stream"),
     ("vec", [synth.batchnorm(C, 3), synth.relu(), synth.maxpool(3, 2, 1)], (3, C, 28, 28), None, "pool_colwalk_vec"),
-    ("vec_avg", [synth.batchnorm(C, 4), synth.relu(), synth.avgpool(2, 2)], (3, C, 14, 14), None, "pool_colwalk_vec"),
+    ("vec_avg", [synth.batchnorm(C, 4), synth.relu(), synth.avgpool(2, 2)], (3, C, 32, 32), None, "pool_colwalk_vec"),
     ("spec", [synth.relu(), synth.maxpool(3, 2)], (3, C, 27, 27), {"force_generic": 2}, "pool_colwalk_spec"),
     ("spec_add", [synth.add(1), synth.relu(), synth.avgpool(3, 2, 1)], (2, C, 13, 13), {"force_generic": 2},
      "pool_colwalk_spec"),
@@ -45,6 +45,9 @@ FAMILIES = [
      "sequence_staged_tma"),
     ("seq_inplace", synth.synthetic51(4, batch=64, C=C, H=20).layers, (64, C, 20, 20), None, "sequence_staged_tma"),
     ("seq_inplace_wide", synth.synthetic51(3, batch=8, C=C, H=100).layers, (8, C, 100, 100), None,
+     "sequence_staged_tma"),
+    # rows of 16 lane groups fill a 16-lane segment: the edge-select (not the -inf pad) in-place step
+    ("seq_inplace_edge", synth.synthetic51(3, batch=8, C=C, H=23).layers, (8, C, 23, 64), None,
      "sequence_staged_tma"),
     ("seq_halo", synth.synthetic51(5, batch=2, C=C, H=64).layers, (2, C, 64, 64), {"force_rows_per_task": 7},
      "sequence_staged_tma"),

@@ -203,3 +203,27 @@ def test_launch_info_reports_smem(cuda_dev):
     sec = synth.synthetic51(3, batch=2, C=3, H=20)
     li = bs.bs_plan_query_launch(bs.bs_plan_create(sec.layers, sec.shape), 0)
     assert li["kernel_name"] == "sequence_staged_tma" and li["smem_bytes"] > 0
+
+
+@pytest.mark.parametrize("variant", ["allneg", "ties", "const", "signed_zero"])
+def test_input_variants_sequences(variant, cuda_dev, oracle_lib):
+    """The variants through the on-chip sequence kernels: the in-place kernel (two-step sweeps with
+    -inf pad lanes, single steps, edge selects), the shared-tile kernel and halo tiles.  Max/ReLU-
+    only sequences are exact (bit for bit modulo the sign of zero); signed-gamma BN ones within
+    tolerance."""
+    for shape in ((2, 4, 28, 28), (1, 4, 56, 56), (1, 2, 23, 64)):
+        n = int(np.prod(shape))
+        x = synth.variant_np(variant, 7, n).reshape(shape)
+        exact = [synth.maxpool(3, 1, 1), synth.relu()] * 3 + [synth.maxpool(3, 1, 1)]
+        affine = []
+        for b in range(5):
+            affine += [synth.maxpool(3, 1, 1), synth.batchnorm(shape[1], 40 + b, signed_gamma=b % 2 == 0), synth.relu()]
+        for layers in (exact, affine):
+            ref = oracle.run_bf(layers, x)
+            for opts in (None, {"force_tile_planes": 1}, {"force_rows_per_task": 5}):
+                got, _ = run_gpu(layers, x, opts=opts)
+                ctx = f"{variant} {shape} {len(layers)} layers {opts}"
+                if not U.needs_tolerance(layers):
+                    U.assert_bitexact(no_zero_sign(got), no_zero_sign(ref), ctx)
+                else:
+                    U.check(got, ref, layers, ctx)

@@ -126,11 +126,13 @@ def test_inplace_kernel_heights(H, cuda_dev, oracle_lib):
     Heights whose parts hold 2, 3, 4, 5 and 28 rows reach every tail of the clean step
     (k_seq.cu inplace_step_clean: W / 4 + 2 lanes fit a segment, H divisible by the parts)."""
     bs = _bs()
-    for W in (4, 16, 56, 64, 68, 112, 128):
+    for W, extra in ((4, 0), (16, 1), (56, 0), (56, 1), (64, 0), (68, 1), (112, 0), (112, 1), (128, 0)):
         shape = (1, 3, H, W)
         layers = [synth.maxpool(3, 1, 1), synth.batchnorm(3, 1, signed_gamma=True), synth.relu(),
                   synth.maxpool(3, 1, 1), synth.relu(), synth.maxpool(3, 1, 1), synth.batchnorm(3, 2),
                   synth.maxpool(3, 1, 1)]
+        # an odd step count: two-step sweeps, then one single step (k_seq.cu inplace_pair_clean)
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(3, 3, signed_gamma=True)] * extra
         x = synth.uniform_np(H * 1000 + W, int(np.prod(shape))).reshape(shape)
         got, plan = run_gpu(layers, x)
         li = bs.bs_plan_query_launch(plan, 0)
