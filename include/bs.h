@@ -146,7 +146,10 @@ typedef struct {
                                        5 = pool vector column walker (stride 2, W % 2 == 0),
                                        6 = pool staged walker (TMA bulk copies of whole planes
                                        into a shared-memory ring), 7 = on-chip multi-step
-                                       sequence (same staging; steps ping-pong in smem) */
+                                       sequence (same staging; steps ping-pong in smem),
+                                       8 = whole-plane pool (window = plane, e.g. a global
+                                       7x7 average): a warp reduces 32 planes, bulk-
+                                       copied (TMA) into its shared-memory slice */
     int32_t first_layer, last_layer;/* layer index range [first, last] covered */
     bs_shape in, out;
     int32_t pool_kh, pool_kw, pool_sh, pool_sw, pool_ph, pool_pw;  /* 0 if no pool */
@@ -158,7 +161,7 @@ typedef struct {
     int32_t halo_rows;              /* kernels 2-6: input rows re-read between row bands (k - s,
                                        >= 0); kernel 7: step-0 input rows loaded in total over a
                                        plane's bands beyond the plane's own rows (redundant halo) */
-    int64_t n_tasks;                /* warp tasks (kernels 2-5), staged tiles (6, 7) */
+    int64_t n_tasks;                /* warp tasks (kernels 2-5, 8), staged tiles (6, 7) */
     int64_t alg_bytes_read, alg_bytes_written;
     int32_t smem_bytes;             /* dynamic shared memory per CTA (0 for kernels 1-5) */
     int32_t tile_planes;            /* kernels 6/7: (n, c) planes per staged tile, else 0 */

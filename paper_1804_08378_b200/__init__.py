@@ -35,7 +35,7 @@ BS_OP = {"batchnorm": 1, "relu": 2, "maxpool": 3, "avgpool": 4, "copy": 5, "scal
          "conv2d": 100, "linear": 101}
 KERNEL_NAMES = {1: "ew_stream", 2: "pool_colwalk_spec", 3: "pool_colwalk_generic", 4: "pool_naive",
                 5: "pool_colwalk_vec", 6: "pool_staged_tma",
-                7: "sequence_staged_tma"}
+                7: "sequence_staged_tma", 8: "pool_planes"}
 
 _FP = ctypes.POINTER(ctypes.c_float)
 

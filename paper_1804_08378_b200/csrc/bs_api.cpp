@@ -301,7 +301,7 @@ void set_device_programs(Launch& l) {
   l.dev_pro = s.pro;
   l.dev_epi = s.epi;
   l.deferred = false;
-  if (l.kernel == K_EW || l.kernel == K_POOL_NAIVE || !max_deferrable(s)) return;
+  if (l.kernel == K_EW || l.kernel == K_POOL_NAIVE || l.kernel == K_POOL_PLANES || !max_deferrable(s)) return;
   l.dev_epi = s.pro;
   l.dev_epi.insert(l.dev_epi.end(), s.epi.begin(), s.epi.end());
   l.dev_pro.clear();
@@ -420,7 +420,13 @@ void configure_step_launch(bs_plan* p, Launch& l, const bs_plan_options& o) {
       const int64_t Wo = s.out.w, Ho = s.out.h;
       const bool per_elem_max = s.is_max && !s.pro.empty() && !max_deferrable(s);
       const int vec = pool_vec_width(s.kh, s.kw, s.sh, s.sw, s.ph, s.pw, (int)s.in.w, (int)Wo);
-      if (s.kw > 32) {
+      if (o.force_generic == 0 && pool_planes_applies((int)s.in.h, (int)s.in.w, s.kh, s.kw, s.ph, s.pw)) {
+        // window = the whole (small) plane: a warp reduces 32 planes (k_pool_planes.cu)
+        l.kernel = K_POOL_PLANES;
+        l.G = 32; l.Jg = 1; l.n_cc = 1; l.gw = 1; l.U = 1;
+        l.rows_per_task = 1;
+        l.n_rb = 1;
+      } else if (s.kw > 32) {
         l.kernel = K_POOL_NAIVE;
       } else if (vec && o.force_generic == 0 && !per_elem_max &&
                  !(!s.is_max && !s.pro.empty() && s.in.w <= 28)) {
@@ -844,12 +850,15 @@ PoolArgs make_pool_args(const bs_plan* p, const Launch& l) {
 int64_t pool_tasks(const Launch& l, int64_t n_planes) {
   if (l.kernel == K_POOL_NAIVE) return n_planes * l.step.out.h * l.step.out.w;
   if (l.kernel == K_POOL_STAGED) return (n_planes + l.tile_planes - 1) / l.tile_planes;   // tiles
+  if (l.kernel == K_POOL_PLANES) return (n_planes + 31) / 32;                              // warp chunks
   return ((n_planes + l.G - 1) / l.G) * l.n_cc * l.n_rb;
 }
 
 int pool_grid(const bs_plan* p, const Launch& l, int64_t n_tasks) {
   if (l.kernel == K_POOL_STAGED)   // persistent: every CTA loops over tiles
     return (int)std::max<int64_t>(1, std::min<int64_t>(n_tasks, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms));
+  if (l.kernel == K_POOL_PLANES)   // one 32-plane chunk per warp, 4 warps per CTA
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n_tasks + 3) / 4, INT32_MAX / 2));
   int64_t g = l.kernel == K_POOL_NAIVE ? (n_tasks + 255) / 256 : (n_tasks + 7) / 8;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, INT32_MAX / 2));
 }
@@ -962,7 +971,8 @@ void fill_launch_info(bs_plan* p) {
       li.halo_rows = std::max(0, s.kh - s.sh);
       li.n_tasks = pool_tasks(l, n_planes);
       li.grid = pool_grid(p, l, li.n_tasks);
-      li.block = l.kernel == K_POOL_STAGED ? kStagedThreads : 256;
+      li.block = l.kernel == K_POOL_STAGED ? kStagedThreads : l.kernel == K_POOL_PLANES ? pool_planes_threads() : 256;
+      if (l.kernel == K_POOL_PLANES) li.smem_bytes = (int32_t)pool_planes_smem((int)(s.in.h * s.in.w));
       if (l.kernel == K_POOL_STAGED) {
         li.smem_bytes = (int32_t)pool_staged_smem(l.tile_planes, (int)(s.in.h * s.in.w), (int)(s.out.h * s.out.w),
                                                   l.stages);
@@ -1217,7 +1227,8 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
       }
       l.blocks_per_sm = bps > 0 ? bps : 5;
       if (l.kernel == K_POOL_STAGED && l.ctas_per_sm > 0) l.blocks_per_sm = std::min(l.blocks_per_sm, l.ctas_per_sm);
-      if (l.kernel != K_POOL_NAIVE && l.kernel != K_POOL_STAGED) size_rows(p, l, o, l.step.in.n * l.step.in.c);
+      if (l.kernel != K_POOL_NAIVE && l.kernel != K_POOL_STAGED && l.kernel != K_POOL_PLANES)
+        size_rows(p, l, o, l.step.in.n * l.step.in.c);
     }
   }
   fill_info(p, shapes, n_layers, n_inputs);

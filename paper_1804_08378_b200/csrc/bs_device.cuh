@@ -326,5 +326,6 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_
 // Kernel pickers of the pool translation units (nullptr: no kernel for this geometry).
 void* pool_fn_global(int kind, const PoolArgs& a);   // K_POOL_SPEC / VEC / GENERIC / NAIVE
 void* pool_fn_staged(const PoolArgs& a);             // K_POOL_STAGED
+void* pool_fn_planes(const PoolArgs& a);             // K_POOL_PLANES
 
 }  // namespace bs

@@ -83,7 +83,7 @@ struct PoolArgs {
 
 // Kernel variants (bs_launch_info.kernel).
 enum KernelKind : int32_t { K_EW = 1, K_POOL_SPEC = 2, K_POOL_GENERIC = 3, K_POOL_NAIVE = 4, K_POOL_VEC = 5,
-                          K_POOL_STAGED = 6, K_SEQ = 7 };
+                          K_POOL_STAGED = 6, K_SEQ = 7, K_POOL_PLANES = 8 };
 
 // ---------------------------------------------------------------- multi-step sequence (NEXT-2)
 // One step of an on-chip sequence: [prologue] pool [epilogue] on the
@@ -168,5 +168,9 @@ __host__ __device__ inline size_t pool_staged_stride(int tile_planes, int HW) {
   return ((size_t)tile_planes * HW * 4 + 16 + 127) / 128 * 128;
 }
 int pool_max_blocks_per_sm(int kernel_kind, const PoolArgs& a, int block);
+// Whole-plane pool kernel (k_pool_planes.cu): whether it applies, its block and dynamic smem.
+bool pool_planes_applies(int H, int W, int kh, int kw, int ph, int pw);
+int pool_planes_threads();
+size_t pool_planes_smem(int HW);
 
 }  // namespace bs

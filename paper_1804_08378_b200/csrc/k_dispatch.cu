@@ -20,6 +20,7 @@ FastDiv make_fastdiv(uint32_t d) {
 
 
 static void* pool_fn(int kind, const PoolArgs& a) {
+  if (kind == K_POOL_PLANES) return pool_fn_planes(a);
   return kind == K_POOL_STAGED ? pool_fn_staged(a) : pool_fn_global(kind, a);
 }
 
@@ -88,6 +89,8 @@ cudaError_t launch_pool(const PoolArgs& a, int kind, int grid, int block, cudaSt
     const size_t smem = pool_staged_smem(a.tile_planes, a.H * a.W, a.Ho * a.Wo, a.stages);
     return launch_pdl(fn, dim3(grid), dim3(kStagedThreads), args, smem, st);
   }
+  if (kind == K_POOL_PLANES)
+    return launch_pdl(fn, dim3(grid), dim3(pool_planes_threads()), args, pool_planes_smem(a.H * a.W), st);
   return launch_pdl(fn, dim3(grid), dim3(kPoolBlock), args, 0, st);
 }
 
@@ -101,6 +104,12 @@ int pool_max_blocks_per_sm(int kind, const PoolArgs& a, int block) {
     const size_t smem = pool_staged_smem(a.tile_planes, a.H * a.W, a.Ho * a.Wo, a.stages);
     if (smem_kernel_setup(fn) != cudaSuccess) return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kStagedThreads, smem) != cudaSuccess) n = 0;
+    return n;
+  }
+  if (kind == K_POOL_PLANES) {
+    const size_t smem = pool_planes_smem(a.H * a.W);
+    if (smem_kernel_setup(fn) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, pool_planes_threads(), smem) != cudaSuccess) n = 0;
     return n;
   }
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kPoolBlock, 0) != cudaSuccess) n = 0;

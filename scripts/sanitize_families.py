@@ -39,8 +39,10 @@ FAMILIES = [
     ("staged_pad", [synth.batchnorm(C, 6, signed_gamma=True), synth.relu(), synth.maxpool(3, 2, 1)],
      (4, C, 21, 23), {"force_generic": 3, "force_stages": 2}, "pool_staged_tma"),
     ("staged_wide", [synth.relu(), synth.maxpool(3, 2)], (1, 2, 5, 1027), {"force_generic": 3}, "pool_staged_tma"),
-    ("staged_avg7", [synth.batchnorm(64, 7), synth.relu(), synth.avgpool(7, 7)], (64, 64, 7, 7), {"force_stages": 2},
-     "pool_staged_tma"),
+    ("staged_avg7", [synth.batchnorm(64, 7), synth.relu(), synth.avgpool(7, 7)], (64, 64, 7, 7),
+     {"force_stages": 2, "force_generic": 3}, "pool_staged_tma"),
+    ("planes", [synth.batchnorm(64, 7), synth.relu(), synth.avgpool(7, 7)], (65, 64, 7, 7), None, "pool_planes"),
+    ("planes_even", [synth.relu(), synth.maxpool(8, 8)], (3, C, 8, 8), None, "pool_planes"),
     ("seq_fast", synth.synthetic51(4, batch=64, C=C, H=20).layers, (64, C, 20, 20), {"force_tile_planes": 1},
      "sequence_staged_tma"),
     ("seq_inplace", synth.synthetic51(4, batch=64, C=C, H=20).layers, (64, C, 20, 20), None, "sequence_staged_tma"),

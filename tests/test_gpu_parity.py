@@ -372,7 +372,8 @@ def test_staged_large_odd_shapes_sampled(shape, pool, cuda_dev, oracle_lib):
     bs = _bs()
     k, s_, p = pool
     layers = [synth.batchnorm(shape[1], 11, signed_gamma=True), synth.relu(), synth.maxpool(k, s_, p)]
-    plan = bs.bs_plan_create(layers, shape)
+    # (a whole-plane window goes to the plane-reduction kernel by default; force the staged one)
+    plan = bs.bs_plan_create(layers, shape, {"force_generic": 3} if k == shape[2] else None)
     assert bs.bs_plan_query_launch(plan, 0)["kernel_name"] == "pool_staged_tma"
     x = synth.uniform_torch(5, shape, device="cuda")
     out = torch.empty(bs.bs_plan_query(plan)["out"], device="cuda")
@@ -423,3 +424,26 @@ def test_ew_large_tensor_rebasing(cuda_dev, oracle_lib):
         # regenerate image n only
         xs = synth.uniform_np(4242, C * 1024 * 1024, start=n * C * 1024 * 1024).reshape(1, C, 1024, 1024)
         U.check(x[n:n + 1].cpu().numpy(), oracle.run_bf(layers, xs), layers, f"image {n}")
+
+
+# ----------------------------------------------------------------------------- whole-plane pools
+@pytest.mark.parametrize("shape", [(3, 5, 7, 7), (2, 7, 8, 8), (1, 3, 5, 5), (2, 33, 4, 4), (1, 40, 1, 1),
+                                   (5, 13, 3, 3), (2, 17, 2, 6), (64, 64, 7, 7)])
+def test_whole_plane_pools(shape, cuda_dev, oracle_lib):
+    """Windows covering the whole plane (global pools, DenseNet-121's final 7x7 average) run the
+    plane-reduction kernel (k_pool_planes.cu): odd / even plane sizes (rotated bank walk), partial
+    32-plane chunks, every prologue class, max with a sign-flipping BN prologue (not deferred)."""
+    bs = _bs()
+    C, H, W = shape[1], shape[2], shape[3]
+    stacks = [[synth.batchnorm(C, 3), synth.relu(), synth.avgpool((H, W), (H, W))],
+              [synth.avgpool((H, W), (H, W))], [synth.relu(), synth.avgpool((H, W), (H, W))],
+              [synth.batchnorm(C, 4, signed_gamma=True), synth.maxpool((H, W), (H, W))],
+              [synth.relu(), synth.maxpool((H, W), (H, W)), synth.batchnorm(C, 5, signed_gamma=True), synth.relu()],
+              [synth.scale(-0.5), synth.avgpool((H, W), (H, W)), synth.scale(3.0)]]
+    x = synth.uniform_np(sum(shape), int(np.prod(shape))).reshape(shape)
+    for layers in stacks:
+        got, plan = compare(layers, x, ctx=f"{shape} {[L.kind for L in layers]}")
+        assert bs.bs_plan_query_launch(plan, 0)["kernel_name"] == "pool_planes"
+        other, _ = run_gpu(layers, x, opts={"force_generic": 1})
+        if not U.needs_tolerance(layers):
+            U.assert_bitexact(got, other, f"{shape} planes vs column walker")
