@@ -223,12 +223,30 @@ BS_API bs_status bs_execute_ex(const bs_plan *plan, const float *const *inputs, 
  *   d_inputs[n_inputs], d_out : caller-owned device buffers of the same shapes (staging).
  *   n_chunks           : the batch is split into n_chunks image ranges; chunk k's
  *                        host->device copy, kernels, and device->host copy are pipelined
- *                        across the plan's two copy streams and `stream` (0 = planner picks).
+ *                        across the plan's two copy streams and `stream` (0 = 8 chunks;
+ *                        at most one chunk per image).
  * Returns after ENQUEUEING; the caller synchronises `stream` before reading h_out.
  */
 BS_API bs_status bs_execute_host(const bs_plan *plan, const float *const *h_inputs, int32_t n_inputs,
                           float *h_out, float *const *d_inputs, float *d_out,
                           int32_t n_chunks, bs_stream_t stream);
+
+/*
+ * bs_execute_host_batch -- bs_execute_host for n_plans executions in array order (a network's
+ * stacks, each from host buffers), pipelined ACROSS executions: execution i+1's host->device
+ * copies start while execution i's kernels and device->host copies are still running, so only
+ * the first copy in and the last copy out of the whole batch are not overlapped (PCIe is full
+ * duplex).  Per execution i: plans[i], h_inputs[i][0..n_inputs[i]), h_outs[i], d_inputs[i][..],
+ * d_outs[i] as in bs_execute_host; n_chunks applies to each execution (0 = planner picks).
+ * The device buffers of different executions must not overlap (BS_ERR_INVALID_ARGUMENT): an
+ * execution's copies may run concurrently with another's kernels.  All plans on one device; the
+ * copy streams and events of the first non-empty plan are used.  Returns after ENQUEUEING; the
+ * caller synchronises `stream` before reading any h_outs[i].  Errors name the execution index.
+ */
+BS_API bs_status bs_execute_host_batch(const bs_plan *const *plans, int32_t n_plans,
+                                       const float *const *const *h_inputs, const int32_t *n_inputs,
+                                       float *const *h_outs, float *const *const *d_inputs,
+                                       float *const *d_outs, int32_t n_chunks, bs_stream_t stream);
 
 /* bs_plan_destroy -- frees plan-owned device memory and streams.  NULL-safe.  The caller
  * must ensure no execution using the plan is still in flight. */

@@ -95,6 +95,9 @@ _lib.bs_execute.argtypes = [_P, _P, _P, _P]
 _lib.bs_execute_ex.argtypes = [_P, ctypes.POINTER(_P), ctypes.c_int32, _P, _P]
 _lib.bs_execute_host.argtypes = [_P, ctypes.POINTER(_P), ctypes.c_int32, _P, ctypes.POINTER(_P), _P,
                                  ctypes.c_int32, _P]
+_lib.bs_execute_host_batch.argtypes = [ctypes.POINTER(_P), ctypes.c_int32, ctypes.POINTER(ctypes.POINTER(_P)),
+                                       ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_P),
+                                       ctypes.POINTER(ctypes.POINTER(_P)), ctypes.POINTER(_P), ctypes.c_int32, _P]
 _lib.bs_graph_create.argtypes = [ctypes.POINTER(_P), ctypes.c_int32, ctypes.POINTER(ctypes.POINTER(_P)),
                                  ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_P), ctypes.POINTER(_P)]
 _lib.bs_graph_create.restype = ctypes.c_int
@@ -109,7 +112,7 @@ _lib.bs_status_string.argtypes = [ctypes.c_int]
 _lib.bs_status_string.restype = ctypes.c_char_p
 _lib.bs_version.restype = ctypes.c_int32
 for _f in ("bs_plan_create", "bs_plan_query", "bs_plan_query_launch", "bs_execute", "bs_execute_ex",
-           "bs_execute_host"):
+           "bs_execute_host", "bs_execute_host_batch"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -251,6 +254,23 @@ def bs_execute_host(plan: Plan, h_inputs: Sequence, h_out, d_inputs: Sequence, d
                                 _stream(stream)), "bs_execute_host")
 
 
+def bs_execute_host_batch(plans: Sequence, h_inputs: Sequence, h_outs: Sequence, d_inputs: Sequence,
+                          d_outs: Sequence, n_chunks: int = 0, stream=None) -> None:
+    """bs_execute_host for several executions, pipelined across them (include/bs.h): per
+    execution i, plans[i], h_inputs[i] (a sequence), h_outs[i], d_inputs[i] (a sequence), d_outs[i]."""
+    n = len(plans)
+    pl = (_P * n)(*[p.handle if isinstance(p, Plan) else p for p in plans])
+    hi_rows = [(_P * len(r))(*[_ptr(t) for t in r]) for r in h_inputs]
+    di_rows = [(_P * len(r))(*[_ptr(t) for t in r]) for r in d_inputs]
+    hi = (ctypes.POINTER(_P) * n)(*[ctypes.cast(r, ctypes.POINTER(_P)) for r in hi_rows])
+    di = (ctypes.POINTER(_P) * n)(*[ctypes.cast(r, ctypes.POINTER(_P)) for r in di_rows])
+    ni = (ctypes.c_int32 * n)(*[len(r) for r in h_inputs])
+    ho = (_P * n)(*[_ptr(t) for t in h_outs])
+    do = (_P * n)(*[_ptr(t) for t in d_outs])
+    _check(_lib.bs_execute_host_batch(pl, n, hi, ni, ho, di, do, int(n_chunks), _stream(stream)),
+           "bs_execute_host_batch")
+
+
 def bs_plan_destroy(plan: Plan) -> None:
     plan.close()
 
@@ -312,5 +332,5 @@ def bs_version() -> int:
 
 
 __all__ = ["bs_plan_create", "bs_plan_query", "bs_plan_query_launch", "bs_execute", "bs_execute_ex",
-           "bs_execute_host", "bs_plan_destroy", "bs_last_error", "bs_status_string", "bs_version", "BsError",
+           "bs_execute_host", "bs_execute_host_batch", "bs_plan_destroy", "bs_last_error", "bs_status_string", "bs_version", "BsError",
            "Plan", "bs_layer_desc", "BS_OP", "KERNEL_NAMES", "LIB_PATH"]

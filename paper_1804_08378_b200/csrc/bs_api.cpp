@@ -121,7 +121,7 @@ struct bs_plan {
   SeqRange* seq_ranges = nullptr;      // device per-band row ranges of on-chip sequences
   float* inter[2] = {nullptr, nullptr};  // intermediates between serialised sequences
   cudaStream_t copy_stream[2] = {nullptr, nullptr};  // bs_execute_host pipelines
-  cudaEvent_t ev_pool[64] = {};
+  cudaEvent_t ev_pool[4] = {};      // bs_execute_host: caller-stream / last-copy / per-chunk events
   int n_events = 0;
 };
 
@@ -1138,6 +1138,87 @@ void free_plan(bs_plan* p) {
 
 }  // namespace
 
+// Host-buffer checks of one bs_execute_host execution.
+bs_status check_host_args(const bs_plan* plan, const float* const* h_inputs, int32_t n_inputs, const float* h_out,
+                          float* const* d_inputs, const float* d_out) {
+  bs_status st = check_exec_args(plan, (const float* const*)d_inputs, n_inputs, d_out);
+  if (st != BS_OK || plan->empty) return st;
+  if (!h_inputs || !h_out) return fail(BS_ERR_INVALID_ARGUMENT, "NULL host pointer");
+  for (int k = 0; k < n_inputs; ++k)
+    if (!h_inputs[k]) return fail(BS_ERR_INVALID_ARGUMENT, "h_inputs[%d] is NULL", k);
+  return BS_OK;
+}
+
+// Bytes of input k of a plan (the stack input, or ADD operand k's layer input / output).
+int64_t input_bytes(const bs_plan* plan, int k) {
+  int64_t nb = plan->launches.front().step.in.numel() * 4;
+  if (k > 0)
+    for (auto& l : plan->launches)
+      for (auto* v : {&l.step.pro, &l.step.epi})
+        for (auto& op : *v)
+          if (op.kind == DOP_ADD && op.operand == k) nb = (v == &l.step.pro ? l.step.in : l.step.out).numel() * 4;
+  return nb;
+}
+
+// Enqueue one execution's chunked pipeline: chunk k's host->device copies on h2d, its kernels on
+// cs (after the copies), its device->host copy on d2h (after the kernels).  The copy streams
+// must already be ordered after whatever they have to follow.  `copied` / `done` are re-recorded
+// per chunk: a stream wait binds the record that is current when the wait is enqueued.
+bs_status pipeline_host(const bs_plan* plan, const float* const* h_inputs, int32_t n_inputs, float* h_out,
+                        float* const* d_inputs, float* d_out, int32_t n_chunks, cudaStream_t cs, cudaStream_t h2d,
+                        cudaStream_t d2h, cudaEvent_t copied, cudaEvent_t done) {
+  const int64_t N = plan->launches.front().step.in.n;
+  // default: 8 chunks (measured on the ResNet-50 step: 2, 8, ~8 MB per chunk and 31 chunks are
+  // within noise of each other and of plain pinned copies of the same bytes -- PCIe-bound)
+  if (n_chunks <= 0) n_chunks = 8;
+  n_chunks = (int32_t)std::min<int64_t>(n_chunks, N);
+  // per-image byte sizes of each input and the output
+  std::vector<int64_t> in_img(n_inputs);
+  for (int k = 0; k < n_inputs; ++k) in_img[k] = input_bytes(plan, k) / N;
+  const int64_t out_img = plan->info.out.c * plan->info.out.h * plan->info.out.w * 4;
+  cudaError_t e = cudaSuccess;
+  for (int32_t k = 0; k < n_chunks && e == cudaSuccess; ++k) {
+    const int64_t i0 = N * k / n_chunks, i1 = N * (k + 1) / n_chunks;
+    for (int q = 0; q < n_inputs && e == cudaSuccess; ++q)
+      e = cudaMemcpyAsync((char*)d_inputs[q] + i0 * in_img[q], (const char*)h_inputs[q] + i0 * in_img[q],
+                          (size_t)((i1 - i0) * in_img[q]), cudaMemcpyHostToDevice, h2d);
+    if (e != cudaSuccess) break;
+    if ((e = cudaEventRecord(copied, h2d)) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(cs, copied, 0)) != cudaSuccess) break;
+    const bs_status st = enqueue(plan, (const float* const*)d_inputs, d_out, i0, i1, cs);
+    if (st != BS_OK) return st;
+    if ((e = cudaEventRecord(done, cs)) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(d2h, done, 0)) != cudaSuccess) break;
+    e = cudaMemcpyAsync((char*)h_out + i0 * out_img, (const char*)d_out + i0 * out_img, (size_t)((i1 - i0) * out_img),
+                        cudaMemcpyDeviceToHost, d2h);
+  }
+  if (e != cudaSuccess) return fail(BS_ERR_CUDA, "bs_execute_host: %s", cudaGetErrorString(e));
+  return BS_OK;
+}
+
+// Runs `body` with the plan's device current, then orders the copy streams after the caller's
+// stream before it and the caller's stream after the last device->host copy.
+template <class F>
+bs_status host_pipeline_scope(const bs_plan* plan, cudaStream_t cs, F body) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != plan->device) cudaSetDevice(plan->device);
+  cudaEvent_t* ev = const_cast<cudaEvent_t*>(plan->ev_pool);
+  cudaStream_t h2d = plan->copy_stream[0], d2h = plan->copy_stream[1];
+  bs_status st = BS_OK;
+  cudaError_t e = cudaEventRecord(ev[0], cs);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, ev[0], 0);
+  if (e == cudaSuccess) st = body(h2d, d2h, ev[2], ev[3]);
+  // the caller's stream completes only after the last device->host copy (also on failure: the
+  // copies already enqueued stay ordered before later work on the caller's stream)
+  if (e == cudaSuccess) e = cudaEventRecord(ev[1], d2h);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[1], 0);
+  if (prev != plan->device) cudaSetDevice(prev);
+  if (st != BS_OK) return st;
+  if (e != cudaSuccess) return fail(BS_ERR_CUDA, "bs_execute_host: %s", cudaGetErrorString(e));
+  return BS_OK;
+}
+
 // ================================================================= extern "C"
 extern "C" {
 
@@ -1312,7 +1393,7 @@ bs_status bs_plan_create(const bs_layer_desc* layers, int32_t n_layers, bs_shape
     }
     for (auto& s : p->copy_stream)
       if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail("cudaStreamCreate", e);
-    p->n_events = 64;
+    p->n_events = 4;
     for (int i = 0; i < p->n_events; ++i)
       if ((e = cudaEventCreateWithFlags(&p->ev_pool[i], cudaEventDisableTiming)) != cudaSuccess) {
         p->n_events = i;
@@ -1357,62 +1438,67 @@ bs_status bs_execute(const bs_plan* plan, const float* in, float* out, bs_stream
 
 bs_status bs_execute_host(const bs_plan* plan, const float* const* h_inputs, int32_t n_inputs, float* h_out,
                           float* const* d_inputs, float* d_out, int32_t n_chunks, bs_stream_t stream) {
-  bs_status st = check_exec_args(plan, (const float* const*)d_inputs, n_inputs, d_out);
+  bs_status st = check_host_args(plan, h_inputs, n_inputs, h_out, d_inputs, d_out);
   if (st != BS_OK || plan->empty) return st;
-  if (!h_inputs || !h_out) return fail(BS_ERR_INVALID_ARGUMENT, "NULL host pointer");
-  for (int k = 0; k < n_inputs; ++k)
-    if (!h_inputs[k]) return fail(BS_ERR_INVALID_ARGUMENT, "h_inputs[%d] is NULL", k);
-  const int64_t N = plan->launches.front().step.in.n;
-  if (n_chunks <= 0) n_chunks = (int32_t)std::min<int64_t>(N, 8);
-  n_chunks = (int32_t)std::min<int64_t>(n_chunks, N);
-  n_chunks = std::min(n_chunks, (plan->n_events - 2) / 2);
-  // kernels of all chunks run in order on `stream`, so plan-owned intermediates are reused safely
-  int prev = 0;
-  cudaGetDevice(&prev);
-  if (prev != plan->device) cudaSetDevice(plan->device);
-  cudaStream_t cs = (cudaStream_t)stream;
-  cudaStream_t h2d = plan->copy_stream[0], d2h = plan->copy_stream[1];
-  // per-image byte sizes of each input and the output
-  std::vector<int64_t> in_img(n_inputs);
-  in_img[0] = plan->launches.front().step.in.numel() / N * 4;
-  for (int k = 1; k < n_inputs; ++k) {
-    for (auto& l : plan->launches)
-      for (auto* v : {&l.step.pro, &l.step.epi})
-        for (auto& op : *v)
-          if (op.kind == DOP_ADD && op.operand == k)
-            in_img[k] = (v == &l.step.pro ? l.step.in : l.step.out).numel() / N * 4;
-  }
-  const int64_t out_img = plan->info.out.c * plan->info.out.h * plan->info.out.w * 4;
-  cudaError_t e = cudaSuccess;
-  cudaEvent_t* ev = const_cast<cudaEvent_t*>(plan->ev_pool);
-  // order the copy streams after prior work on the caller's stream
-  e = cudaEventRecord(ev[0], cs);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, ev[0], 0);
-  for (int32_t k = 0; k < n_chunks && e == cudaSuccess; ++k) {
-    const int64_t i0 = N * k / n_chunks, i1 = N * (k + 1) / n_chunks;
-    for (int q = 0; q < n_inputs && e == cudaSuccess; ++q)
-      e = cudaMemcpyAsync((char*)d_inputs[q] + i0 * in_img[q], (const char*)h_inputs[q] + i0 * in_img[q],
-                          (size_t)((i1 - i0) * in_img[q]), cudaMemcpyHostToDevice, h2d);
-    if (e != cudaSuccess) break;
-    cudaEvent_t copied = ev[2 + 2 * k], done = ev[3 + 2 * k];
-    if ((e = cudaEventRecord(copied, h2d)) != cudaSuccess) break;
-    if ((e = cudaStreamWaitEvent(cs, copied, 0)) != cudaSuccess) break;
-    st = enqueue(plan, (const float* const*)d_inputs, d_out, i0, i1, cs);
+  return host_pipeline_scope(plan, (cudaStream_t)stream, [&](cudaStream_t h2d, cudaStream_t d2h, cudaEvent_t c,
+                                                             cudaEvent_t d) {
+    return pipeline_host(plan, h_inputs, n_inputs, h_out, d_inputs, d_out, n_chunks, (cudaStream_t)stream, h2d, d2h,
+                         c, d);
+  });
+}
+
+bs_status bs_execute_host_batch(const bs_plan* const* plans, int32_t n_plans, const float* const* const* h_inputs,
+                                const int32_t* n_inputs, float* const* h_outs, float* const* const* d_inputs,
+                                float* const* d_outs, int32_t n_chunks, bs_stream_t stream) {
+  if (n_plans < 0 || (n_plans > 0 && (!plans || !h_inputs || !n_inputs || !h_outs || !d_inputs || !d_outs)))
+    return fail(BS_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (n_plans == 0) return BS_OK;
+  const bs_plan* lead = nullptr;
+  for (int32_t i = 0; i < n_plans; ++i) {
+    bs_status st = check_host_args(plans[i], h_inputs[i], n_inputs[i], h_outs[i], d_inputs[i], d_outs[i]);
     if (st != BS_OK) {
-      if (prev != plan->device) cudaSetDevice(prev);
-      return st;
+      const std::string m = bs_last_error();
+      return fail(st, "execution %d: %s", i, m.c_str());
     }
-    if ((e = cudaEventRecord(done, cs)) != cudaSuccess) break;
-    if ((e = cudaStreamWaitEvent(d2h, done, 0)) != cudaSuccess) break;
-    e = cudaMemcpyAsync((char*)h_out + i0 * out_img, (const char*)d_out + i0 * out_img, (size_t)((i1 - i0) * out_img),
-                        cudaMemcpyDeviceToHost, d2h);
+    if (plans[i]->empty) continue;
+    if (!lead) lead = plans[i];
+    if (plans[i]->device != lead->device) return fail(BS_ERR_INVALID_ARGUMENT, "execution %d: plans on different devices", i);
   }
-  // the caller's stream completes only after the last device->host copy
-  if (e == cudaSuccess) e = cudaEventRecord(ev[1], d2h);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[1], 0);
-  if (prev != plan->device) cudaSetDevice(prev);
-  if (e != cudaSuccess) return fail(BS_ERR_CUDA, "bs_execute_host: %s", cudaGetErrorString(e));
-  return BS_OK;
+  if (!lead) return BS_OK;
+  // an execution's host->device copies may overlap earlier executions' kernels and copies, so the
+  // device buffers of different executions must not overlap
+  for (int32_t i = 0; i < n_plans; ++i) {
+    if (plans[i]->empty) continue;
+    for (int32_t j = 0; j < i; ++j) {
+      if (plans[j]->empty) continue;
+      auto bufs = [&](int32_t x, std::vector<std::pair<const void*, size_t>>& v) {
+        v.clear();
+        for (int k = 0; k < n_inputs[x]; ++k) v.push_back({d_inputs[x][k], (size_t)input_bytes(plans[x], k)});
+        const bs_shape& o = plans[x]->info.out;
+        v.push_back({d_outs[x], (size_t)(o.n * o.c * o.h * o.w) * 4});
+      };
+      std::vector<std::pair<const void*, size_t>> bi, bj;
+      bufs(i, bi);
+      bufs(j, bj);
+      for (auto& x : bi)
+        for (auto& y : bj)
+          if (overlaps(x.first, x.second, y.first, y.second))
+            return fail(BS_ERR_INVALID_ARGUMENT, "executions %d and %d share device buffers", j, i);
+    }
+  }
+  return host_pipeline_scope(lead, (cudaStream_t)stream, [&](cudaStream_t h2d, cudaStream_t d2h, cudaEvent_t c,
+                                                             cudaEvent_t d) {
+    for (int32_t i = 0; i < n_plans; ++i) {
+      if (plans[i]->empty) continue;
+      const bs_status st = pipeline_host(plans[i], h_inputs[i], n_inputs[i], h_outs[i], d_inputs[i], d_outs[i],
+                                         n_chunks, (cudaStream_t)stream, h2d, d2h, c, d);
+      if (st != BS_OK) {
+        const std::string m = bs_last_error();
+        return fail(st, "execution %d: %s", i, m.c_str());
+      }
+    }
+    return BS_OK;
+  });
 }
 
 void bs_plan_destroy(bs_plan* plan) { free_plan(plan); }

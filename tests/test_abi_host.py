@@ -31,7 +31,7 @@ def header_symbols():
 
 def test_exports_every_declared_symbol(bs):
     syms = header_symbols()
-    assert len(syms) == 13, syms   # 10 + bs_graph_create / _launch / _destroy (NEXT-3)
+    assert len(syms) == 14, syms   # 10 + bs_graph_create / _launch / _destroy (NEXT-3) + bs_execute_host_batch
     out = subprocess.check_output(["nm", "-D", "--defined-only", bs.LIB_PATH]).decode()
     exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
     for s in syms:

@@ -296,6 +296,43 @@ def test_execute_host_matches_device(cuda_dev, oracle_lib):
             U.check(h_out.numpy(), oracle.run_bf(layers, x, ops), layers, f"host chunks={chunks}")
 
 
+def test_execute_host_batch_matches_oracle(cuda_dev, oracle_lib):
+    """bs_execute_host_batch: several stacks (one with an ADD operand, one sequence, one empty)
+    from host buffers in one pipelined call, each checked against the oracle; device buffers
+    shared between executions are rejected with the execution indices named."""
+    bs = _bs()
+    specs = [([synth.batchnorm(6, 1), synth.relu(), synth.maxpool(3, 2, 1)], (7, 6, 21, 19), 0),
+             ([synth.batchnorm(5, 2), synth.add(1), synth.relu()], (9, 5, 7, 7), 1),
+             (synth.synthetic51(4, batch=3, C=4, H=24).layers, (3, 4, 24, 24), 0),
+             ([synth.relu(), synth.maxpool(2, 2)], (0, 3, 8, 8), 0),
+             ([synth.batchnorm(64, 3), synth.relu(), synth.avgpool(7, 7)], (16, 64, 7, 7), 0)]
+    plans, h_ins, h_outs, d_ins, d_outs, refs = [], [], [], [], [], []
+    for k, (layers, shape, nops) in enumerate(specs):
+        if shape[0]:
+            x, ops = U.make_inputs(layers, shape, nops, 20 + k, oracle.layer_shapes(layers, shape, nops))
+        else:   # the empty batch: a no-op execution in the batch
+            x, ops = np.zeros(shape, np.float32), []
+        plan = bs.bs_plan_create(layers, shape)
+        info = bs.bs_plan_query(plan)
+        plans.append(plan)
+        h_ins.append([torch.from_numpy(a).pin_memory() for a in [x] + ops])
+        h_outs.append(torch.full(info["out"], float("nan")).pin_memory())
+        d_ins.append([torch.empty_like(t, device="cuda") for t in h_ins[-1]])
+        d_outs.append(torch.empty(info["out"], device="cuda"))
+        refs.append((layers, oracle.run_bf(layers, x, ops) if shape[0] else None))
+    for chunks in (0, 1, 4):
+        for h in h_outs:
+            h.fill_(float("nan"))
+        bs.bs_execute_host_batch(plans, h_ins, h_outs, d_ins, d_outs, chunks)
+        torch.cuda.synchronize()
+        for (layers, ref), h in zip(refs, h_outs):
+            if ref is not None:
+                U.check(h.numpy(), ref, layers, f"batch chunks={chunks}")
+    with pytest.raises(bs.BsError, match="executions 0 and 2"):
+        bs.bs_execute_host_batch(plans[:3], h_ins[:3], h_outs[:3], d_ins[:3], [d_outs[0], d_outs[1], d_outs[0]])
+    bs.bs_execute_host_batch([], [], [], [], [])
+
+
 def test_inplace_elementwise(cuda_dev, oracle_lib):
     bs = _bs()
     shape = (2, 6, 13, 13)
