@@ -605,16 +605,21 @@ int64_t inplace_smem(const std::vector<Step>& steps, size_t a, size_t b, const b
                      int64_t* stage_out = nullptr, int64_t* stages_out = nullptr, int64_t* planes_out = nullptr) {
   if (o.force_tile_planes > 0 || o.force_rows_per_task > 0 || b - a > (size_t)kMaxSeqSteps) return -1;
   const int64_t W = steps[a].in.w, H = steps[a].in.h;
-  if (W > 128) return -1;
+  if (W > 224) return -1;
   for (size_t k = a; k < b; ++k)
     if (!is_fast_step(steps[k]) || steps[k].in.w != W || steps[k].in.h != H) return -1;
+  // planes 129..224 wide: one plane per CTA, 8 warps each owning H / 8 rows of both column
+  // segments of the row (k_seq.cu seq_inplace<32, true, 2>); only with equal parts of >= 2 rows
+  const bool wide = W > 128;
+  if (wide && (H % 8 != 0 || H < 16)) return -1;
+  const int64_t warps = wide ? 8 : kInplaceWarps;
   // planes per CTA: warps per plane chosen so that ~4 CTAs (16 consumer warps) fit an SM: small
   // planes one warp each, 112 x 112 planes four warps each
-  int64_t P = kInplaceWarps;
+  int64_t P = wide ? 1 : kInplaceWarps;
   while (P > 1 && 4 * (P * H * W * 4 + 2048) > 220 * 1024) P /= 2;
   const int64_t stage = (P * H * W * 4 + 16 + 127) / 128 * 128;
-  const int64_t S = o.force_stages >= 1 ? std::min<int64_t>(kStagedMaxStages, o.force_stages) : 1;
-  const int64_t smem = 128 + S * stage + (int64_t)kInplaceWarps * (int64_t)(b - a) * 8 + 1024;
+  const int64_t S = wide ? 1 : o.force_stages >= 1 ? std::min<int64_t>(kStagedMaxStages, o.force_stages) : 1;
+  const int64_t smem = 128 + S * stage + warps * (int64_t)(b - a) * 8 + 1024;
   if (stage_out) *stage_out = stage;
   if (stages_out) *stages_out = S;
   if (planes_out) *planes_out = P;
@@ -954,7 +959,7 @@ void fill_launch_info(bs_plan* p) {
       li.rows_per_task = (int32_t)s.out.h;
       li.n_tasks = (n_planes + l.tile_planes - 1) / l.tile_planes * l.seq_bands;   // tiles
       li.grid = (int)std::min<int64_t>(li.n_tasks, (int64_t)std::max(1, l.blocks_per_sm) * p->num_sms);
-      li.block = l.seq_inplace_seg ? 32 * (kInplaceWarps + 1) : kSeqThreads;
+      li.block = l.seq_inplace_seg ? seq_inplace_threads(seq_probe(l)) : kSeqThreads;
       li.smem_bytes = (int32_t)(l.seq_inplace_seg ? seq_inplace_smem(seq_probe(l)) : seq_smem(seq_probe(l)));
       li.tile_planes = l.tile_planes;
       li.tile_rows = l.seq_bands > 1 ? l.seq_band_rows : 0;

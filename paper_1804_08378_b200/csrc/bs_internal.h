@@ -135,6 +135,7 @@ constexpr int kInplaceWarps = 4;   // consumer warps per CTA of seq_inplace (1, 
 cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st);
 size_t seq_smem(const SeqArgs& a);
 size_t seq_inplace_smem(const SeqArgs& a);
+int seq_inplace_threads(const SeqArgs& a);
 int seq_max_blocks_per_sm(const SeqArgs& a);
 
 // Launchers (k_*.cu).  Return the launch error (cudaSuccess on success).

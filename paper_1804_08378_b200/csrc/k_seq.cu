@@ -454,23 +454,64 @@ __device__ __forceinline__ void inplace_step(uint32_t pbase, float* og, int H, i
   else __syncwarp();
 }
 
-// The same step for the common shapes (56 x 56 and 112 x 112 planes): every part has the same
-// Hp >= 2 rows (H % parts == 0) and a row of W / 4 lane groups leaves a free lane on either side
-// of it in its segment (W / 4 + 2 <= SEG).  Column group g sits on lane g + 1; the free (pad)
-// lanes read -inf (PadLd) and never store, so the outer neighbours of the plane's edge columns
-// arrive by the same two shuffles as every other column's -- no edge selects, no predicated loads.  Rows below the part are never
-// touched inside the loop (no address clamps): the main loop stops two rows before the part's
-// end, the last two rows take the own last row and the row saved below.  Per 4 outputs and row:
-// LDS.128, 2 SHFL, 8 FMNMX3, the epilogue, STS.128 (STG.128 on the last step), one address add.
-template <int SEG, bool LAST, int EPI>
-__device__ __forceinline__ void inplace_step_clean(uint32_t pbase, PadLd ld, float* og, int H, int W, bool st_ok,
+// The same step for the common shapes (56 x 56, 112 x 112 and 224 x 224 planes): every part has
+// the same Hp >= 2 rows (H % parts == 0) and a lane segment holds its column groups with a free
+// lane on either side.  Column group g of segment s sits on lane g - first(s) + 1; the side
+// lanes hold the neighbouring group of the next segment (a halo, read only) or, at the plane's
+// edges, -inf (PadLd: the max identity); neither stores.  So the outer neighbours of every
+// column arrive by the same two shuffles -- no edge selects, no predicated loads.  NSEG = 2
+// segments (planes 129..224 wide, 8 warps per plane) cover a row with 2 x 28 groups; one warp
+// walks both in lockstep, so a row is read (both segments, halos included) before it is
+// overwritten.  Rows below the part are never touched inside the loop (no address clamps): the
+// main loop stops two rows before the part's end, the last two rows take the own last row and
+// the row saved below.  Per 4 outputs and row: LDS.128, 2 SHFL, 8 FMNMX3, the epilogue,
+// STS.128 (STG.128 on the last step), one address add.
+template <int N>
+struct Vec4 {
+  float4 s[N];
+};
+// A lane's segments: byte offset of segment s's column from segment 0's, its loads (pad lanes
+// redirected to -inf), whether it holds plane data and whether it stores.
+template <int N>
+struct SegLanes {
+  uint32_t off[N];
+  PadLd ld[N];
+  bool col_ok[N], st_ok[N];
+};
+
+template <int SEG, int N>
+__device__ __forceinline__ Vec4<N> seg_hraw(const Vec4<N>& x) {
+  Vec4<N> h;
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    const float4 v = x.s[q];
+    const float l = __shfl_up_sync(0xffffffffu, v.w, 1, SEG);
+    const float rr = __shfl_down_sync(0xffffffffu, v.x, 1, SEG);
+    h.s[q] = make_float4(max3f(l, v.x, v.y), max3f(v.x, v.y, v.z), max3f(v.y, v.z, v.w), max3f(v.z, v.w, rr));
+  }
+  return h;
+}
+template <int N>
+__device__ __forceinline__ Vec4<N> seg_ld(const SegLanes<N>& L, uint32_t a) {
+  Vec4<N> v;
+#pragma unroll
+  for (int q = 0; q < N; ++q) v.s[q] = L.ld[q](q ? a + L.off[q] : a);
+  return v;
+}
+template <bool LAST, int N>
+__device__ __forceinline__ void seg_store(const SegLanes<N>& L, uint32_t ad, float* og, const Vec4<N>& o) {
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+    if (L.st_ok[q]) {
+      if (LAST) st_stream4(q ? og + L.off[q] / 4 : og, o.s[q]);
+      else sts128(q ? ad + L.off[q] : ad, o.s[q]);
+    }
+}
+
+template <int SEG, int N, bool LAST, int EPI>
+__device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLanes<N>& L, float* og, int H, int W,
                                                    float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
   const uint32_t W4 = 4u * (uint32_t)W;
-  auto hraw = [&](const float4& x) -> float4 {
-    const float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
-    const float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
-    return make_float4(max3f(l, x.x, x.y), max3f(x.x, x.y, x.z), max3f(x.y, x.z, x.w), max3f(x.z, x.w, rr));
-  };
   auto epi = [&](float v) -> float {
     if (EPI >= 2) v = __fmaf_rn(v, aff.x, aff.y);
     if (EPI == 1 || EPI == 3) v = relu(v);
@@ -478,31 +519,31 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, PadLd ld, flo
   };
   uint32_t ad = pbase + (uint32_t)r0 * W4;
   // everything this part reads from outside its own rows, before any part writes
-  const float4 x_bound = ld(r0 + Hp < H ? ad + (uint32_t)Hp * W4 : ad + (uint32_t)(Hp - 1) * W4);
-  float4 hA = hraw(ld(r0 > 0 ? ad - W4 : ad));   // the row above (a duplicate at the top edge)
-  float4 hB = hraw(ld(ad));
-  float4 x1 = ld(ad + W4);                        // raw row r0 + 1 (Hp >= 2: the part's own)
+  const Vec4<N> x_bound = seg_ld(L, r0 + Hp < H ? ad + (uint32_t)Hp * W4 : ad + (uint32_t)(Hp - 1) * W4);
+  Vec4<N> hA = seg_hraw<SEG>(seg_ld(L, r0 > 0 ? ad - W4 : ad));   // the row above (a duplicate at the top)
+  Vec4<N> hB = seg_hraw<SEG>(seg_ld(L, ad));
+  Vec4<N> x1 = seg_ld(L, ad + W4);                                // raw row r0 + 1 (Hp >= 2: the part's own)
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();                                 // the other half-warp's part
   float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
-  float4 hC;
-  auto out = [&](const float4& a, const float4& b, const float4& c) {
-    float4 o;
-    o.x = epi(max3f(a.x, b.x, c.x));
-    o.y = epi(max3f(a.y, b.y, c.y));
-    o.z = epi(max3f(a.z, b.z, c.z));
-    o.w = epi(max3f(a.w, b.w, c.w));
-    if (st_ok) {
-      if (LAST) st_stream4(o_g, o);
-      else sts128(ad, o);
+  Vec4<N> hC;
+  auto out = [&](const Vec4<N>& a, const Vec4<N>& b, const Vec4<N>& c) {
+    Vec4<N> o;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      o.s[q].x = epi(max3f(a.s[q].x, b.s[q].x, c.s[q].x));
+      o.s[q].y = epi(max3f(a.s[q].y, b.s[q].y, c.s[q].y));
+      o.s[q].z = epi(max3f(a.s[q].z, b.s[q].z, c.s[q].z));
+      o.s[q].w = epi(max3f(a.s[q].w, b.s[q].w, c.s[q].w));
     }
+    seg_store<LAST>(L, ad, o_g, o);
     if (LAST) o_g += W;
     ad += W4;
   };
   // output row i (i + 2 < Hp): raw row i + 2 is loaded before row i is overwritten
-  auto row = [&](const float4& a, const float4& b, float4& nx) {
-    const float4 x2 = ld(ad + 2u * W4);
-    nx = hraw(x1);
+  auto row = [&](const Vec4<N>& a, const Vec4<N>& b, Vec4<N>& nx) {
+    const Vec4<N> x2 = seg_ld(L, ad + 2u * W4);
+    nx = seg_hraw<SEG>(x1);
     x1 = x2;
     out(a, b, nx);
   };
@@ -516,17 +557,17 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, PadLd ld, flo
   // 0..2 main rows left, then the part's last two rows (own row Hp - 1 in x1, then the row below)
   const int rem = n_main - i;
   if (rem == 0) {
-    hC = hraw(x1);       out(hA, hB, hC);
-    hA = hraw(x_bound);  out(hB, hC, hA);
+    hC = seg_hraw<SEG>(x1);       out(hA, hB, hC);
+    hA = seg_hraw<SEG>(x_bound);  out(hB, hC, hA);
   } else if (rem == 1) {
     row(hA, hB, hC);
-    hA = hraw(x1);       out(hB, hC, hA);
-    hB = hraw(x_bound);  out(hC, hA, hB);
+    hA = seg_hraw<SEG>(x1);       out(hB, hC, hA);
+    hB = seg_hraw<SEG>(x_bound);  out(hC, hA, hB);
   } else {
     row(hA, hB, hC);
     row(hB, hC, hA);
-    hB = hraw(x1);       out(hC, hA, hB);
-    hC = hraw(x_bound);  out(hA, hB, hC);
+    hB = seg_hraw<SEG>(x1);       out(hC, hA, hB);
+    hC = seg_hraw<SEG>(x_bound);  out(hA, hB, hC);
   }
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();
@@ -540,63 +581,67 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, PadLd ld, flo
 // g[i - 1 .. i + 1] over raw row i, which nothing needs any more.  The part's edges need two raw
 // rows on either side (read before any part writes) and one redundant y row on either side; at
 // the plane's top / bottom edge the step-k row beyond the plane is absent, i.e. g[-1] := g[0] and
-// g[H] := g[H - 1] (duplicates, exact for max).  Epilogues are branch-free per step: v * s + t
-// then max(v, lo), with (s, t) = (1, -0) without BN (exact: v + -0 == v, -0 included) and
-// lo = -inf without ReLU.  The window rotates through three register roles (no moves): the main
-// loop is unrolled by 3 and the part's last 2..5 rows are unrolled per remainder.
-template <int SEG, bool LAST>
-__device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, PadLd ld, float* og, int H, int W, bool col_ok,
-                                                   bool st_ok, float2 a1, float lo1, float2 a2, float lo2, int r0,
-                                                   int Hp, int bar_id, int bar_threads) {
+// g[H] := g[H - 1] (duplicates, exact for max).  A halo lane's step-k value is exact for its
+// inner column (its neighbour inside the segment is real), the only one the segment needs.
+// Epilogues are branch-free per step: v * s + t then max(v, lo), with (s, t) = (1, -0) without
+// BN (exact: v + -0 == v, -0 included) and lo = -inf without ReLU.  The window rotates through
+// three register roles (no moves): the main loop is unrolled by 3 and the part's last 2..5 rows
+// are unrolled per remainder.
+template <int SEG, int N, bool LAST>
+__device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLanes<N>& L, float* og, int H, int W,
+                                                   float2 a1, float lo1, float2 a2, float lo2, int r0, int Hp,
+                                                   int bar_id, int bar_threads) {
   const uint32_t W4 = 4u * (uint32_t)W;
-  auto hraw = [&](const float4& x) -> float4 {
-    const float l = __shfl_up_sync(0xffffffffu, x.w, 1, SEG);
-    const float rr = __shfl_down_sync(0xffffffffu, x.x, 1, SEG);
-    return make_float4(max3f(l, x.x, x.y), max3f(x.x, x.y, x.z), max3f(x.y, x.z, x.w), max3f(x.z, x.w, rr));
-  };
-  auto vert = [&](const float4& a, const float4& b, const float4& c, float2 s, float lo) -> float4 {
-    float4 o;
-    o.x = fmaxf(__fmaf_rn(max3f(a.x, b.x, c.x), s.x, s.y), lo);
-    o.y = fmaxf(__fmaf_rn(max3f(a.y, b.y, c.y), s.x, s.y), lo);
-    o.z = fmaxf(__fmaf_rn(max3f(a.z, b.z, c.z), s.x, s.y), lo);
-    o.w = fmaxf(__fmaf_rn(max3f(a.w, b.w, c.w), s.x, s.y), lo);
-    return o;
-  };
   // A pad lane's step-k row must stay -inf (its neighbours take it as their outer column), but its
   // horizontal maxima pick up the edge columns through the shuffles: (s, t) = (0, -inf) maps any
   // finite v to -inf and -inf to NaN, which max(., lo = -inf) turns back into -inf.
-  if (!col_ok) { a1 = make_float2(0.f, -CUDART_INF_F); lo1 = -CUDART_INF_F; }
+  float2 a1s[N];
+  float lo1s[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    a1s[q] = L.col_ok[q] ? a1 : make_float2(0.f, -CUDART_INF_F);
+    lo1s[q] = L.col_ok[q] ? lo1 : -CUDART_INF_F;
+  }
+  auto vert = [&](const Vec4<N>& a, const Vec4<N>& b, const Vec4<N>& c, bool first) -> Vec4<N> {
+    Vec4<N> o;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const float2 s = first ? a1s[q] : a2;
+      const float lo = first ? lo1s[q] : lo2;
+      o.s[q].x = fmaxf(__fmaf_rn(max3f(a.s[q].x, b.s[q].x, c.s[q].x), s.x, s.y), lo);
+      o.s[q].y = fmaxf(__fmaf_rn(max3f(a.s[q].y, b.s[q].y, c.s[q].y), s.x, s.y), lo);
+      o.s[q].z = fmaxf(__fmaf_rn(max3f(a.s[q].z, b.s[q].z, c.s[q].z), s.x, s.y), lo);
+      o.s[q].w = fmaxf(__fmaf_rn(max3f(a.s[q].w, b.s[q].w, c.s[q].w), s.x, s.y), lo);
+    }
+    return o;
+  };
   const bool top = r0 == 0, bot = r0 + Hp == H;
   uint32_t ad = pbase + (uint32_t)r0 * W4;
   // rows outside the part, before any part writes (clamped copies at the plane's edges)
-  const float4 xa2 = ld(top ? ad : ad - 2u * W4);
-  const float4 xa1 = ld(top ? ad : ad - W4);
-  const float4 xb1 = ld(bot ? ad + (uint32_t)(Hp - 1) * W4 : ad + (uint32_t)Hp * W4);
-  const float4 xb2 = ld(bot ? ad + (uint32_t)(Hp - 1) * W4 : ad + (uint32_t)(Hp + 1) * W4);
-  const float4 x0 = ld(ad), x1 = ld(ad + W4);
-  float4 xn = Hp > 2 ? ld(ad + 2u * W4) : xb1;   // raw row r0 + 2, one row ahead
+  const Vec4<N> xa2 = seg_ld(L, top ? ad : ad - 2u * W4);
+  const Vec4<N> xa1 = seg_ld(L, top ? ad : ad - W4);
+  const Vec4<N> xb1 = seg_ld(L, bot ? ad + (uint32_t)(Hp - 1) * W4 : ad + (uint32_t)Hp * W4);
+  const Vec4<N> xb2 = seg_ld(L, bot ? ad + (uint32_t)(Hp - 1) * W4 : ad + (uint32_t)(Hp + 1) * W4);
+  const Vec4<N> x0 = seg_ld(L, ad), x1 = seg_ld(L, ad + W4);
+  Vec4<N> xn = Hp > 2 ? seg_ld(L, ad + 2u * W4) : xb1;   // raw row r0 + 2, one row ahead
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();
-  float4 hA = hraw(x0), hB = hraw(x1), hC;
-  float4 gA, gB, gC;
+  Vec4<N> hA = seg_hraw<SEG>(x0), hB = seg_hraw<SEG>(x1), hC;
+  Vec4<N> gA, gB, gC;
   {
-    const float4 hm2 = hraw(xa2), hm1 = hraw(xa1);
-    gA = hraw(vert(hm2, hm1, hA, a1, lo1));           // g[r0 - 1]
-    gB = hraw(vert(hm1, hA, hB, a1, lo1));            // g[r0]
+    const Vec4<N> hm2 = seg_hraw<SEG>(xa2), hm1 = seg_hraw<SEG>(xa1);
+    gA = seg_hraw<SEG>(vert(hm2, hm1, hA, true));     // g[r0 - 1]
+    gB = seg_hraw<SEG>(vert(hm1, hA, hB, true));      // g[r0]
     if (top) gA = gB;
   }
   float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
   // z row i from the window; x = raw row i + 2
-  auto row = [&](const float4& x, const float4& ha, const float4& hb, float4& hc, const float4& ga, const float4& gb,
-                 float4& gc, bool bottom_row) {
-    hc = hraw(x);
-    gc = hraw(vert(ha, hb, hc, a1, lo1));
+  auto row = [&](const Vec4<N>& x, const Vec4<N>& ha, const Vec4<N>& hb, Vec4<N>& hc, const Vec4<N>& ga,
+                 const Vec4<N>& gb, Vec4<N>& gc, bool bottom_row) {
+    hc = seg_hraw<SEG>(x);
+    gc = seg_hraw<SEG>(vert(ha, hb, hc, true));
     if (bottom_row) gc = gb;
-    const float4 o = vert(ga, gb, gc, a2, lo2);
-    if (st_ok) {
-      if (LAST) st_stream4(o_g, o);
-      else sts128(ad, o);
-    }
+    seg_store<LAST>(L, ad, o_g, vert(ga, gb, gc, false));
     if (LAST) o_g += W;
     ad += W4;
   };
@@ -607,9 +652,9 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, PadLd ld, flo
   int i = 0;
   // main rows: the prefetched row i + 3 is the part's own
   for (; i + 3 <= Hp - 3; i += 3) {
-    float4 x = xn; xn = ld(ad + 3u * W4); BS_ROW0(x, false);
-    x = xn; xn = ld(ad + 3u * W4);        BS_ROW1(x, false);
-    x = xn; xn = ld(ad + 3u * W4);        BS_ROW2(x, false);
+    Vec4<N> x = xn; xn = seg_ld(L, ad + 3u * W4); BS_ROW0(x, false);
+    x = xn; xn = seg_ld(L, ad + 3u * W4);         BS_ROW1(x, false);
+    x = xn; xn = seg_ld(L, ad + 3u * W4);         BS_ROW2(x, false);
   }
   // r own-prefetch rows left (r = Hp - 3 - i in {-1 (Hp == 2), 0, 1, 2}), then the part's last
   // three rows, which take own row Hp - 1 (prefetched), the row below, the row after it
@@ -622,13 +667,13 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, PadLd ld, flo
     BS_ROW1(xb1, false);
     BS_ROW2(xb2, bot);
   } else if (r == 1) {
-    float4 x = xn; xn = ld(ad + 3u * W4); BS_ROW0(x, false);
+    Vec4<N> x = xn; xn = seg_ld(L, ad + 3u * W4); BS_ROW0(x, false);
     BS_ROW1(xn, false);
     BS_ROW2(xb1, false);
     BS_ROW0(xb2, bot);
   } else {
-    float4 x = xn; xn = ld(ad + 3u * W4); BS_ROW0(x, false);
-    x = xn; xn = ld(ad + 3u * W4);        BS_ROW1(x, false);
+    Vec4<N> x = xn; xn = seg_ld(L, ad + 3u * W4); BS_ROW0(x, false);
+    x = xn; xn = seg_ld(L, ad + 3u * W4);         BS_ROW1(x, false);
     BS_ROW2(xn, false);
     BS_ROW0(xb1, false);
     BS_ROW1(xb2, bot);
@@ -640,18 +685,19 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, PadLd ld, flo
   else __syncwarp();
 }
 
-template <int SEG, bool CLEAN, bool LAST>
-__device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, PadLd W4, float* og, int H, int W, int c,
-                                                 bool st_ok, float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
+template <int SEG, bool CLEAN, int N, bool LAST>
+__device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, const SegLanes<N>& L, float* og, int H, int W,
+                                                 int c, float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
   if (CLEAN) {
     switch (epi) {
-      case 0: inplace_step_clean<SEG, LAST, 0>(base, W4, og, H, W, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
-      case 1: inplace_step_clean<SEG, LAST, 1>(base, W4, og, H, W, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
-      case 2: inplace_step_clean<SEG, LAST, 2>(base, W4, og, H, W, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
-      default: inplace_step_clean<SEG, LAST, 3>(base, W4, og, H, W, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
+      case 0: inplace_step_clean<SEG, N, LAST, 0>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
+      case 1: inplace_step_clean<SEG, N, LAST, 1>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
+      case 2: inplace_step_clean<SEG, N, LAST, 2>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
+      default: inplace_step_clean<SEG, N, LAST, 3>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
     }
     return;
   }
+  const bool st_ok = L.st_ok[0];
   switch (epi) {
     case 0: inplace_step<SEG, LAST, 0>(base, og, H, W, c, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
     case 1: inplace_step<SEG, LAST, 1>(base, og, H, W, c, st_ok, aff, r0, Hp, bar_id, bar_threads); break;
@@ -660,14 +706,21 @@ __device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, PadLd W
   }
 }
 
+// Consumer warps of seq_inplace: 4 (planes <= 128 wide, 1 - 4 per tile), 8 for the two-segment
+// rows of planes 129..224 wide (one plane per tile, one CTA per SM).
+__host__ __device__ constexpr int inplace_warps_of(int nseg) { return nseg == 2 ? 8 : kInplaceWarps; }
+__host__ __device__ inline int inplace_nseg(int W) { return W > 128 ? 2 : 1; }
+
 // Whether seq_inplace takes the clean step (inplace_step_clean) for these planes.
 __host__ __device__ inline bool inplace_clean(int seg, int tile_planes, int H, int W) {
+  if (inplace_nseg(W) == 2) return true;   // planned only when clean (bs_api.cpp inplace_smem)
   const int parts = (kInplaceWarps / tile_planes) * (32 / seg);
   return W / 4 + 2 <= seg && H % parts == 0 && H / parts >= 2;
 }
 
-template <int SEG, bool CLEAN>
-__global__ void __launch_bounds__(32 * (kInplaceWarps + 1), 4) seq_inplace(SeqArgs a) {
+template <int SEG, bool CLEAN, int NSEG>
+__global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ? 1 : 4) seq_inplace(SeqArgs a) {
+  constexpr int WARPS = inplace_warps_of(NSEG);
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int8_t epi_tab[kMaxSeqSteps];
   __shared__ const float2* aff_tab[kMaxSeqSteps];
@@ -682,7 +735,7 @@ __global__ void __launch_bounds__(32 * (kInplaceWarps + 1), 4) seq_inplace(SeqAr
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 2);
-      mbar_init(&empty[s], 32 * kInplaceWarps);
+      mbar_init(&empty[s], 32 * WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -727,17 +780,19 @@ __global__ void __launch_bounds__(32 * (kInplaceWarps + 1), 4) seq_inplace(SeqAr
     return;
   }
 
-  // warps_per_plane (= kInplaceWarps / tile_planes) consumer warps share a plane; its rows are cut
-  // into warps_per_plane * 32/SEG parts, one per half-warp (16-lane segments) or warp
+  // warps_per_plane (= WARPS / tile_planes) consumer warps share a plane; its rows are cut into
+  // warps_per_plane * 32/SEG parts, one per half-warp (16-lane segments) or warp
   const int cw = warp - 1;
-  const int wpp = kInplaceWarps / a.tile_planes;
+  const int wpp = WARPS / a.tile_planes;
   const int sl = lane & (SEG - 1), half = lane / SEG;
-  const int c = 4 * (CLEAN ? sl - 1 : sl);            // clean: lane 0 of a segment is a -inf pad
+  const int c = 4 * (CLEAN ? sl - 1 : sl);            // clean: lane 0 of a segment is a -inf pad / halo
   const int part = (cw % wpp) * (32 / SEG) + half;
   const int n_parts = wpp * (32 / SEG);
   const int Hp = (H + n_parts - 1) / n_parts;
   const int bar_id = wpp > 1 ? 1 + cw / wpp : 0;       // named barrier of the plane's warps
   float2* const t_aff = (float2*)(stage0 + (size_t)a.stages * a.stage_bytes) + (size_t)cw * n;   // this warp's
+  // column segments: NSEG = 2 splits a row's W / 4 groups into two halves of GS groups
+  const int GS = NSEG == 2 ? (W / 4 + 1) / 2 : 0;
   int k = 0;
   for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
     const int s = k % a.stages;
@@ -751,58 +806,68 @@ __global__ void __launch_bounds__(32 * (kInplaceWarps + 1), 4) seq_inplace(SeqAr
     for (int i = lane; i < n; i += 32) t_aff[i] = aff_tab[i] ? __ldg(aff_tab[i] + ch) : make_float2(1.f, -0.f);
     __syncwarp();
     mbar_wait_sleep(&full[s], (k / a.stages) & 1);
-    const bool st_ok = p < np && c >= 0 && c < W;
     const char* sbase = (const char*)stage0 + (size_t)s * a.stage_bytes +
                         ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW) & 15u);
-    // clean: pad lanes read the -inf float4 at every row (row pitch 0) and never store
-    const bool col_ok = c >= 0 && c < W;
     const uint32_t base = smem_u32(sbase) + 4u * (uint32_t)(min(p, np - 1) * HW + c);
-    const PadLd W4{col_ok ? ~0u : 127u, col_ok ? 0u : smem_u32(s_ninf)};
     float* og = a.out + (int64_t)plane * HW + c;
+    // this lane's segments: pad lanes (outside the plane) read -inf and never store; halo lanes
+    // (the neighbouring segment's edge group) read and never store
+    SegLanes<NSEG> L;
+#pragma unroll
+    for (int q = 0; q < NSEG; ++q) {
+      const int cq = c + 4 * q * GS;                    // this lane's column in segment q
+      L.off[q] = 16u * (uint32_t)(q * GS);
+      L.col_ok[q] = cq >= 0 && cq < W;
+      L.st_ok[q] = p < np && L.col_ok[q] && (NSEG == 1 || (sl >= 1 && sl <= GS));
+      L.ld[q] = PadLd{L.col_ok[q] ? ~0u : 127u, L.col_ok[q] ? 0u : smem_u32(s_ninf)};
+    }
     int st = 0;
     if (CLEAN) {   // steps two at a time (one sweep per pair), an odd last step alone
       for (; st + 1 < n; st += 2) {
         const float lo1 = (epi_tab[st] & 1) ? 0.f : -CUDART_INF_F, lo2 = (epi_tab[st + 1] & 1) ? 0.f : -CUDART_INF_F;
         if (st + 2 == n)
-          inplace_pair_clean<SEG, true>(base, W4, og, H, W, col_ok, st_ok, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp,
-                                        Hp, bar_id, 32 * wpp);
+          inplace_pair_clean<SEG, NSEG, true>(base, L, og, H, W, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp, Hp,
+                                              bar_id, 32 * wpp);
         else
-          inplace_pair_clean<SEG, false>(base, W4, og, H, W, col_ok, st_ok, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp,
-                                         Hp, bar_id, 32 * wpp);
+          inplace_pair_clean<SEG, NSEG, false>(base, L, og, H, W, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp, Hp,
+                                               bar_id, 32 * wpp);
       }
     }
     for (; st < n; ++st) {
       const float2 aff = t_aff[st];
       if (st == n - 1)
-        inplace_step_epi<SEG, CLEAN, true>(epi_tab[st], base, W4, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
+        inplace_step_epi<SEG, CLEAN, NSEG, true>(epi_tab[st], base, L, og, H, W, c, aff, part * Hp, Hp, bar_id, 32 * wpp);
       else
-        inplace_step_epi<SEG, CLEAN, false>(epi_tab[st], base, W4, og, H, W, c, st_ok, aff, part * Hp, Hp, bar_id, 32 * wpp);
+        inplace_step_epi<SEG, CLEAN, NSEG, false>(epi_tab[st], base, L, og, H, W, c, aff, part * Hp, Hp, bar_id, 32 * wpp);
     }
     mbar_arrive(&empty[s]);   // every lane: the tile's stage is free for the producer
   }
 }
 
+int seq_inplace_threads(const SeqArgs& a) { return 32 * (inplace_warps_of(inplace_nseg(a.W0)) + 1); }
+
 size_t seq_inplace_smem(const SeqArgs& a) {
-  return 128 + (size_t)a.stages * a.stage_bytes + (size_t)kInplaceWarps * a.n_steps * 8 + 1024;
+  return 128 + (size_t)a.stages * a.stage_bytes + (size_t)inplace_warps_of(inplace_nseg(a.W0)) * a.n_steps * 8 + 1024;
 }
 
 static const void* seq_fn(const SeqArgs& a) {
+  if (a.inplace_seg && inplace_nseg(a.W0) == 2) return (const void*)seq_inplace<32, true, 2>;
   const bool clean = a.inplace_seg && inplace_clean(a.inplace_seg, a.tile_planes, a.H0, a.W0);
-  if (a.inplace_seg == 16) return clean ? (const void*)seq_inplace<16, true> : (const void*)seq_inplace<16, false>;
-  if (a.inplace_seg == 32) return clean ? (const void*)seq_inplace<32, true> : (const void*)seq_inplace<32, false>;
+  if (a.inplace_seg == 16) return clean ? (const void*)seq_inplace<16, true, 1> : (const void*)seq_inplace<16, false, 1>;
+  if (a.inplace_seg == 32) return clean ? (const void*)seq_inplace<32, true, 1> : (const void*)seq_inplace<32, false, 1>;
   return (const void*)seq_staged;
 }
 
 cudaError_t launch_seq(const SeqArgs& a, int grid, cudaStream_t st) {
   void* args[] = {(void*)&a};
   if (a.inplace_seg)
-    return launch_pdl(seq_fn(a), dim3(grid), dim3(32 * (kInplaceWarps + 1)), args, seq_inplace_smem(a), st);
+    return launch_pdl(seq_fn(a), dim3(grid), dim3(seq_inplace_threads(a)), args, seq_inplace_smem(a), st);
   return launch_pdl((void*)seq_staged, dim3(grid), dim3(kSeqThreads), args, seq_smem(a), st);
 }
 
 int seq_max_blocks_per_sm(const SeqArgs& a) {
   const size_t smem = a.inplace_seg ? seq_inplace_smem(a) : seq_smem(a);
-  const int threads = a.inplace_seg ? 32 * (kInplaceWarps + 1) : kSeqThreads;
+  const int threads = a.inplace_seg ? seq_inplace_threads(a) : kSeqThreads;
   int n = 0;
   if (smem_kernel_setup(seq_fn(a)) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, seq_fn(a), threads, smem) != cudaSuccess) n = 0;

@@ -39,7 +39,7 @@ for spec in "resnet50 0" "alexnet 0" "vgg16 0" "densenet121 11"; do
   $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
        --log-file $O/traffic_$1_$2.csv python scripts/prof_one.py $1 $2 3 > $O/traffic_$1_$2.log 2>&1
 done
-for spec in "resnet50 0 pool_vec" "alexnet 0 pool_staged" "densenet121 11 ew_kernel"; do
+for spec in "resnet50 0 pool_vec" "alexnet 0 pool_staged" "densenet121 11 ew_kernel" "densenet121 -1 pool_planes"; do
   set -- $spec
   $NCU --set full --clock-control none --import-source on -k regex:$3 -s 1 -c 1 -o /tmp/full_$1_$2 -f \
        python scripts/prof_one.py $1 $2 3 > $O/full_$1_$2.log 2>&1

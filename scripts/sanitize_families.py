@@ -48,6 +48,9 @@ FAMILIES = [
     ("seq_inplace", synth.synthetic51(4, batch=64, C=C, H=20).layers, (64, C, 20, 20), None, "sequence_staged_tma"),
     ("seq_inplace_wide", synth.synthetic51(3, batch=8, C=C, H=100).layers, (8, C, 100, 100), None,
      "sequence_staged_tma"),
+    # planes 129..224 wide: one plane per CTA, two column segments per row with halo lanes
+    ("seq_inplace_2seg", synth.synthetic51(3, batch=2, C=C, H=16).layers, (2, C, 16, 160), None,
+     "sequence_staged_tma"),
     # rows of 16 lane groups fill a 16-lane segment: the edge-select (not the -inf pad) in-place step
     ("seq_inplace_edge", synth.synthetic51(3, batch=8, C=C, H=23).layers, (8, C, 23, 64), None,
      "sequence_staged_tma"),

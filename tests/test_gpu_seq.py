@@ -141,3 +141,25 @@ def test_inplace_kernel_heights(H, cuda_dev, oracle_lib):
         other, plan2 = run_gpu(layers, x, {"force_tile_planes": 1})
         assert bs.bs_plan_query_launch(plan2, 0)["block"] != 160
         U.assert_bitexact(got, other, f"H={H} W={W} in-place vs shared tile")
+
+
+@pytest.mark.parametrize("H,W", [(16, 132), (24, 200), (40, 160), (56, 224), (224, 224)])
+def test_inplace_wide_planes(H, W, cuda_dev, oracle_lib):
+    """Planes 129..224 wide run in place too (k_seq.cu seq_inplace<32, true, 2>): one plane per CTA,
+    8 warps of H / 8 rows, each row as two column segments with halo lanes; even and odd step
+    counts (two-step sweeps + a single step), signed-gamma BN; bit for bit equal to the
+    shared-tile / halo kernels (force_tile_planes routes there) and within tolerance of the oracle."""
+    bs = _bs()
+    for extra in (0, 1):
+        shape = (2, 3, H, W)
+        layers = [synth.maxpool(3, 1, 1), synth.batchnorm(3, 1, signed_gamma=True), synth.relu(),
+                  synth.maxpool(3, 1, 1), synth.relu(), synth.maxpool(3, 1, 1), synth.batchnorm(3, 2),
+                  synth.maxpool(3, 1, 1)] + [synth.maxpool(3, 1, 1), synth.batchnorm(3, 3, signed_gamma=True)] * extra
+        x = synth.uniform_np(H * 1000 + W + extra, int(np.prod(shape))).reshape(shape)
+        got, plan = run_gpu(layers, x)
+        li = bs.bs_plan_query_launch(plan, 0)
+        assert li["block"] == 288 and li["tile_planes"] == 1 and li["stages"] == 1, li
+        assert li["smem_bytes"] < 1.5 * H * W * 4, li                         # in place: no work buffer
+        U.assert_close(got, oracle.run_bf(layers, x), f"H={H} W={W} extra={extra}")
+        other, _ = run_gpu(layers, x, {"force_tile_planes": 1})
+        U.assert_bitexact(got, other, f"H={H} W={W} in-place vs shared tile / halo")
