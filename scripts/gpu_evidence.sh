@@ -27,6 +27,8 @@ if [ -z "$NOSEC" ]; then
 timeout 900 python scripts/exp_sec51.py $O/sec51_56.jsonl 128 64 56 1,2,4,8,12,16,17,20,24,32,40 > /dev/null 2> $O/sec51_56.err
 timeout 900 python scripts/exp_sec51.py $O/sec51_112.jsonl 64 64 112 1,5,16,32,40 --no-eager > /dev/null 2> $O/sec51_112.err
 timeout 900 python scripts/exp_sec51.py $O/sec51_224.jsonl 32 64 224 1,5,8,15,16,30,40 --no-eager > /dev/null 2> $O/sec51_224.err
+# the paper's cache-limit artifact: 224^2 planes under a 110 KB budget -> halo tiles
+BS_SEC51_OPTS='{"smem_budget_bytes": 112640}' timeout 900 python scripts/exp_sec51.py $O/sec51_224_budget110k.jsonl 32 64 224 1,5,8,14,15,16,30,40 --no-eager > /dev/null 2> $O/sec51_224_budget.err
 fi
 if [ -z "$NONCU" ]; then
 # launch list of a short default bench (cold-cache, serialised: compare shares)

@@ -96,13 +96,18 @@ def test_sequence_packing(bs, depth, policy, seqs):
 
 
 def test_large_planes_use_halo_tiles(bs):
-    """Planes too large to hold whole in shared memory are fused with halo (row-band) tiles."""
+    """Planes too large to hold whole in shared memory are fused with halo (row-band) tiles: planes
+    wider than the in-place kernel's 224 columns, or 224 x 224 planes under a 110 KB budget."""
     layers = [synth.maxpool(3, 1, 1), synth.relu(), synth.maxpool(3, 1, 1)]
-    p = host_plan(bs, layers, (1, 2, 224, 224))
-    info = bs.bs_plan_query(p)
-    li = bs.bs_plan_query_launch(p, 0)
-    assert info["n_sequences"] == 1 and li["kernel_name"] == "sequence_staged_tma"
-    assert 0 < li["tile_rows"] < 224 and li["halo_rows"] > 0
+    for shape, opts in (((1, 2, 240, 240), {}), ((1, 2, 224, 224), {"smem_budget_bytes": 110 * 1024})):
+        p = host_plan(bs, layers, shape, **opts)
+        info = bs.bs_plan_query(p)
+        li = bs.bs_plan_query_launch(p, 0)
+        assert info["n_sequences"] == 1 and li["kernel_name"] == "sequence_staged_tma"
+        assert 0 < li["tile_rows"] < shape[2] and li["halo_rows"] > 0
+    # 224 x 224 within the default budget: whole planes, in place (one plane per CTA, 8 warps)
+    li = bs.bs_plan_query_launch(host_plan(bs, layers, (1, 2, 224, 224)), 0)
+    assert li["tile_rows"] == 0 and li["halo_rows"] == 0 and li["block"] == 288 and li["tile_planes"] == 1
     p = host_plan(bs, layers, (1, 2, 56, 56))
     li = bs.bs_plan_query_launch(p, 0)
     assert bs.bs_plan_query(p)["n_sequences"] == 1 and li["tile_rows"] == 0 and li["halo_rows"] == 0
@@ -130,21 +135,21 @@ def _sec51_split_depth(W, H, budget=110 * 1024, lanes=256):
         d = n
 
 
-@pytest.mark.parametrize("H,depth", [(224, 40), (112, 70), (160, 40)])
-def test_halo_sequence_split_depth(bs, H, depth):
-    """'Unrestricted' (-1) §5.1 networks on large planes split where the growing halo band overflows
+@pytest.mark.parametrize("H,depth,budget", [(224, 40, 110 * 1024), (112, 70, 48 * 1024), (160, 40, 96 * 1024),
+                                            (240, 40, 0)])
+def test_halo_sequence_split_depth(bs, H, depth, budget):
+    """'Unrestricted' (-1) §5.1 networks on planes that do not fit whole under the budget (the in-place
+    kernel needs one H x H plane per CTA, > budget here) split where the growing halo band overflows
     the shared-memory budget (the paper's cache-limit artifacts), at the depth the
     closed form gives -- not at a fixed step limit."""
     layers = []
     for b in range(depth):
         layers += [synth.maxpool(3, 1, 1), synth.batchnorm(4, b), synth.relu()]
-    p = host_plan(bs, layers, (2, 4, H, H), max_steps_per_sequence=-1)
+    opts = {"smem_budget_bytes": budget} if budget else {}
+    assert H * H * 4 > (budget or 220 * 1024) or H > 224
+    p = host_plan(bs, layers, (2, 4, H, H), max_steps_per_sequence=-1, **opts)
     info = bs.bs_plan_query(p)
-    d = _sec51_split_depth(H, H)
-    whole = 128 + 2 * (-(-(H * H * 4 + 16) // 128) * 128) + H * H * 4 + 1024 <= 220 * 1024
-    if whole:
-        assert info["n_sequences"] == -(-depth // 64)
-        return
+    d = _sec51_split_depth(H, H, budget or 110 * 1024)
     assert info["n_sequences"] == -(-depth // d), (d, info)
     li = bs.bs_plan_query_launch(p, 0)
     assert li["groups_per_warp"] == d and li["tile_rows"] >= -(-256 // H)
@@ -352,16 +357,17 @@ def test_wide_plane_plans(bs, shape, layers):
     assert li["smem_bytes"] >= 128 + li["stages"] * li["tile_planes"] * shape[2] * shape[3] * 4
 
 
-@pytest.mark.parametrize("H", [224, 160, 300])
-def test_default_policy_bounds_halo(bs, H):
+@pytest.mark.parametrize("H,budget", [(224, 110 * 1024), (160, 96 * 1024), (240, 0), (300, 0)])
+def test_default_policy_bounds_halo(bs, H, budget):
     """The planner's default (0) stops a halo-tiled sequence once the band no longer covers its
     own input halo: every sequence has halo rows <= band rows per band, and one more step would
-    break that (or not fit)."""
+    break that (or not fit).  (Planes that do not fit whole under the budget: halo tiles.)"""
     depth = 40
     layers = []
     for b in range(depth):
         layers += [synth.maxpool(3, 1, 1), synth.batchnorm(4, b), synth.relu()]
-    p = host_plan(bs, layers, (2, 4, H, H))
+    opts = {"smem_budget_bytes": budget} if budget else {}
+    p = host_plan(bs, layers, (2, 4, H, H), **opts)
     info = bs.bs_plan_query(p)
     assert 1 < info["n_sequences"] < depth
     for k in range(info["n_launches"]):
@@ -371,7 +377,7 @@ def test_default_policy_bounds_halo(bs, H):
         n_bands = -(-H // li["tile_rows"])
         assert li["halo_rows"] <= n_bands * li["tile_rows"], li
         assert 2 * li["groups_per_warp"] <= li["tile_rows"] + 2, li   # 2 halo rows per 3x3/p1 step
-    unres = bs.bs_plan_query(host_plan(bs, layers, (2, 4, H, H), max_steps_per_sequence=-1))
+    unres = bs.bs_plan_query(host_plan(bs, layers, (2, 4, H, H), max_steps_per_sequence=-1, **opts))
     assert unres["n_sequences"] <= info["n_sequences"]
 
 
