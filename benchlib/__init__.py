@@ -33,19 +33,23 @@ def lib():
         _lib = ctypes.CDLL(LIB)
         _lib.bsc_ldg.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                  ctypes.c_void_p]
+        _lib.bsc_flat.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                  ctypes.c_void_p]
         _lib.bsc_ring.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
     return _lib
 
 
 # variants timed per stack; the ceiling is the fastest
-VARIANTS = [("ldg", 4), ("ldg", 8), ("ring", 16384, 4, 2), ("ring", 32768, 3, 2)]
+VARIANTS = [("ldg", 4), ("ldg", 8), ("flat", 1), ("flat", 4), ("ring", 16384, 4, 2), ("ring", 32768, 3, 2)]
 
 
 def launch(variant, in_ptr: int, n_in: int, out_ptr: int, n_out: int, stream: int) -> None:
     L = lib()
     if variant[0] == "ldg":
         rc = L.bsc_ldg(in_ptr, n_in, out_ptr, n_out, variant[1], stream)
+    elif variant[0] == "flat":
+        rc = L.bsc_flat(in_ptr, n_in, out_ptr, n_out, variant[1], stream)
     else:
         rc = L.bsc_ring(in_ptr, n_in, out_ptr, n_out, variant[1], variant[2], variant[3], stream)
     if rc:

@@ -4,9 +4,11 @@
 // work -- so a stack's time can be reported against the best a streaming kernel achieves for the
 // same byte counts and read/write mix on this GPU (launch ramp and drain included).
 //
-// Two variants (bench.py takes the faster per stack):
+// Three variants (bench.py takes the fastest per stack):
 //   bsc_ldg  : flat grid-stride; per iteration 4 x LDG.128 in flight per thread
 //              (ld.global.nc.L1::no_allocate), then the proportional share of STG.128 (.cs).
+//   bsc_flat : one block per 256 x U float4s, no loop: U loads in flight per thread, then the
+//              block's proportional output share (for equal sizes: a plain copy kernel).
 //   bsc_ring : persistent CTAs; one elected lane bulk-copies (cp.async.bulk, TMA) input tiles into
 //              a shared-memory ring behind mbarriers, 8 consumer warps read each tile and write
 //              its proportional share of the output.
@@ -55,6 +57,29 @@ __global__ void __launch_bounds__(256) k_ldg(const float4* __restrict__ in, int6
     for (int64_t o = o0 + g; o < o1; o += T) stcs4(out + o, acc);
   }
   if (g == 0) tails(in1, n_in, out1, n_out, acc);
+}
+
+// Flat: one block per 256 * U float4s of the input (no grid-stride loop): each thread loads its U
+// float4s (all in flight), then the block writes its proportional share of the output at the
+// matching position -- for n_out == n_in exactly a copy kernel, for a pool's 4:1 ratio the
+// streaming pattern of a one-pass pool kernel.
+template <int U>
+__global__ void __launch_bounds__(256) k_flat(const float4* __restrict__ in, int64_t n4i, float4* __restrict__ out,
+                                              int64_t n4o, const float* in1, int64_t n_in, float* out1, int64_t n_out) {
+  const int64_t b0 = (int64_t)blockIdx.x * 256 * U;
+  float acc = -CUDART_INF_F;
+  float4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = b0 + u * 256 + threadIdx.x;
+    v[u] = i < n4i ? ldnc4(in + i) : make_float4(acc, acc, acc, acc);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc = fmaxf(acc, mx4(v[u]));
+  const int64_t b1 = b0 + 256 * U < n4i ? b0 + 256 * U : n4i;
+  const int64_t o0 = (int64_t)((double)b0 * n4o / n4i), o1 = (int64_t)((double)b1 * n4o / n4i);
+  for (int64_t o = o0 + threadIdx.x; o < o1; o += 256) stcs4(out + o, acc);
+  if (blockIdx.x == 0 && threadIdx.x == 0) tails(in1, n_in, out1, n_out, acc);
 }
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -140,6 +165,17 @@ __attribute__((visibility("default"))) int bsc_ldg(const float* in, int64_t n_in
   const int64_t need = (n4i + 1023) / 1024;   // at least one float4 per thread per iteration
   if (need < grid) grid = need < 1 ? 1 : need;
   k_ldg<<<(int)grid, 256, 0, st>>>((const float4*)in, n4i, (float4*)out, n_out / 4, in, n_in, out, n_out);
+  return (int)cudaGetLastError();
+}
+
+__attribute__((visibility("default"))) int bsc_flat(const float* in, int64_t n_in, float* out, int64_t n_out,
+                                                    int unroll, cudaStream_t st) {
+  const int64_t n4i = n_in / 4;
+  const int64_t per = 256 * (int64_t)unroll;
+  const int grid = (int)(n4i > 0 ? (n4i + per - 1) / per : 1);
+  if (unroll == 1) k_flat<1><<<grid, 256, 0, st>>>((const float4*)in, n4i, (float4*)out, n_out / 4, in, n_in, out, n_out);
+  else if (unroll == 2) k_flat<2><<<grid, 256, 0, st>>>((const float4*)in, n4i, (float4*)out, n_out / 4, in, n_in, out, n_out);
+  else k_flat<4><<<grid, 256, 0, st>>>((const float4*)in, n4i, (float4*)out, n_out / 4, in, n_in, out, n_out);
   return (int)cudaGetLastError();
 }
 
