@@ -320,6 +320,19 @@ def test_execute_host_batch_matches_oracle(cuda_dev, oracle_lib):
         d_ins.append([torch.empty_like(t, device="cuda") for t in h_ins[-1]])
         d_outs.append(torch.empty(info["out"], device="cuda"))
         refs.append((layers, oracle.run_bf(layers, x, ops) if shape[0] else None))
+    # the same plan twice (a network's repeated stacks) on its own buffers; and a two-sequence plan
+    layers = [synth.relu(), synth.maxpool(3, 2, 1), synth.batchnorm(4, 9), synth.maxpool(2, 2)]
+    for k, (ls, shape) in enumerate([(specs[0][0], specs[0][1]), (layers, (3, 4, 30, 30))]):
+        x, _ = U.make_inputs(ls, shape, 0, 40 + k, oracle.layer_shapes(ls, shape, 0))
+        plan = plans[0] if k == 0 else bs.bs_plan_create(ls, shape, {"max_steps_per_sequence": 1})
+        info = bs.bs_plan_query(plan)
+        plans.append(plan)
+        h_ins.append([torch.from_numpy(x).pin_memory()])
+        h_outs.append(torch.full(info["out"], float("nan")).pin_memory())
+        d_ins.append([torch.empty_like(h_ins[-1][0], device="cuda")])
+        d_outs.append(torch.empty(info["out"], device="cuda"))
+        refs.append((ls, oracle.run_bf(ls, x)))
+    assert bs.bs_plan_query(plans[-1])["n_launches"] == 2
     for chunks in (0, 1, 4):
         for h in h_outs:
             h.fill_(float("nan"))
