@@ -471,35 +471,42 @@ struct Vec4 {
   float4 s[N];
 };
 // A lane's segments: byte offset of segment s's column from segment 0's, its loads (pad lanes
-// redirected to -inf), whether it holds plane data and whether it stores.
-template <int N>
+// redirected to -inf), whether it holds plane data and whether it stores.  E (edge selects): rows
+// that fill their segment have no free lanes for -inf pads; the plane's edge columns then take
+// their missing neighbour from themselves (a duplicate, exact for max; le / re mark those lanes).
+template <int N, bool E = false>
 struct SegLanes {
   uint32_t off[N];
   PadLd ld[N];
   bool col_ok[N], st_ok[N];
+  bool le[N], re[N];
 };
 
-template <int SEG, int N>
-__device__ __forceinline__ Vec4<N> seg_hraw(const Vec4<N>& x) {
+template <int SEG, int N, bool E>
+__device__ __forceinline__ Vec4<N> seg_hraw(const Vec4<N>& x, const SegLanes<N, E>& L) {
   Vec4<N> h;
 #pragma unroll
   for (int q = 0; q < N; ++q) {
     const float4 v = x.s[q];
-    const float l = __shfl_up_sync(0xffffffffu, v.w, 1, SEG);
-    const float rr = __shfl_down_sync(0xffffffffu, v.x, 1, SEG);
+    float l = __shfl_up_sync(0xffffffffu, v.w, 1, SEG);
+    float rr = __shfl_down_sync(0xffffffffu, v.x, 1, SEG);
+    if (E) {
+      l = L.le[q] ? v.x : l;
+      rr = L.re[q] ? v.w : rr;
+    }
     h.s[q] = make_float4(max3f(l, v.x, v.y), max3f(v.x, v.y, v.z), max3f(v.y, v.z, v.w), max3f(v.z, v.w, rr));
   }
   return h;
 }
-template <int N>
-__device__ __forceinline__ Vec4<N> seg_ld(const SegLanes<N>& L, uint32_t a) {
+template <int N, bool E>
+__device__ __forceinline__ Vec4<N> seg_ld(const SegLanes<N, E>& L, uint32_t a) {
   Vec4<N> v;
 #pragma unroll
   for (int q = 0; q < N; ++q) v.s[q] = L.ld[q](q ? a + L.off[q] : a);
   return v;
 }
-template <bool LAST, int N>
-__device__ __forceinline__ void seg_store(const SegLanes<N>& L, uint32_t ad, float* og, const Vec4<N>& o) {
+template <bool LAST, int N, bool E>
+__device__ __forceinline__ void seg_store(const SegLanes<N, E>& L, uint32_t ad, float* og, const Vec4<N>& o) {
 #pragma unroll
   for (int q = 0; q < N; ++q)
     if (L.st_ok[q]) {
@@ -508,8 +515,8 @@ __device__ __forceinline__ void seg_store(const SegLanes<N>& L, uint32_t ad, flo
     }
 }
 
-template <int SEG, int N, bool LAST, int EPI>
-__device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLanes<N>& L, float* og, int H, int W,
+template <int SEG, int N, bool LAST, int EPI, bool E>
+__device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLanes<N, E>& L, float* og, int H, int W,
                                                    float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
   const uint32_t W4 = 4u * (uint32_t)W;
   auto epi = [&](float v) -> float {
@@ -520,8 +527,8 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
   uint32_t ad = pbase + (uint32_t)r0 * W4;
   // everything this part reads from outside its own rows, before any part writes
   const Vec4<N> x_bound = seg_ld(L, r0 + Hp < H ? ad + (uint32_t)Hp * W4 : ad + (uint32_t)(Hp - 1) * W4);
-  Vec4<N> hA = seg_hraw<SEG>(seg_ld(L, r0 > 0 ? ad - W4 : ad));   // the row above (a duplicate at the top)
-  Vec4<N> hB = seg_hraw<SEG>(seg_ld(L, ad));
+  Vec4<N> hA = seg_hraw<SEG>(seg_ld(L, r0 > 0 ? ad - W4 : ad), L);   // the row above (a duplicate at the top)
+  Vec4<N> hB = seg_hraw<SEG>(seg_ld(L, ad), L);
   Vec4<N> x1 = seg_ld(L, ad + W4);                                // raw row r0 + 1 (Hp >= 2: the part's own)
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();                                 // the other half-warp's part
@@ -543,7 +550,7 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
   // output row i (i + 2 < Hp): raw row i + 2 is loaded before row i is overwritten
   auto row = [&](const Vec4<N>& a, const Vec4<N>& b, Vec4<N>& nx) {
     const Vec4<N> x2 = seg_ld(L, ad + 2u * W4);
-    nx = seg_hraw<SEG>(x1);
+    nx = seg_hraw<SEG>(x1, L);
     x1 = x2;
     out(a, b, nx);
   };
@@ -557,17 +564,17 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
   // 0..2 main rows left, then the part's last two rows (own row Hp - 1 in x1, then the row below)
   const int rem = n_main - i;
   if (rem == 0) {
-    hC = seg_hraw<SEG>(x1);       out(hA, hB, hC);
-    hA = seg_hraw<SEG>(x_bound);  out(hB, hC, hA);
+    hC = seg_hraw<SEG>(x1, L);       out(hA, hB, hC);
+    hA = seg_hraw<SEG>(x_bound, L);  out(hB, hC, hA);
   } else if (rem == 1) {
     row(hA, hB, hC);
-    hA = seg_hraw<SEG>(x1);       out(hB, hC, hA);
-    hB = seg_hraw<SEG>(x_bound);  out(hC, hA, hB);
+    hA = seg_hraw<SEG>(x1, L);       out(hB, hC, hA);
+    hB = seg_hraw<SEG>(x_bound, L);  out(hC, hA, hB);
   } else {
     row(hA, hB, hC);
     row(hB, hC, hA);
-    hB = seg_hraw<SEG>(x1);       out(hC, hA, hB);
-    hC = seg_hraw<SEG>(x_bound);  out(hA, hB, hC);
+    hB = seg_hraw<SEG>(x1, L);       out(hC, hA, hB);
+    hC = seg_hraw<SEG>(x_bound, L);  out(hA, hB, hC);
   }
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();
@@ -587,8 +594,8 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
 // BN (exact: v + -0 == v, -0 included) and lo = -inf without ReLU.  The window rotates through
 // three register roles (no moves): the main loop is unrolled by 3 and the part's last 2..5 rows
 // are unrolled per remainder.
-template <int SEG, int N, bool LAST>
-__device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLanes<N>& L, float* og, int H, int W,
+template <int SEG, int N, bool LAST, bool E>
+__device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLanes<N, E>& L, float* og, int H, int W,
                                                    float2 a1, float lo1, float2 a2, float lo2, int r0, int Hp,
                                                    int bar_id, int bar_threads) {
   const uint32_t W4 = 4u * (uint32_t)W;
@@ -626,20 +633,20 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLane
   Vec4<N> xn = Hp > 2 ? seg_ld(L, ad + 2u * W4) : xb1;   // raw row r0 + 2, one row ahead
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();
-  Vec4<N> hA = seg_hraw<SEG>(x0), hB = seg_hraw<SEG>(x1), hC;
+  Vec4<N> hA = seg_hraw<SEG>(x0, L), hB = seg_hraw<SEG>(x1, L), hC;
   Vec4<N> gA, gB, gC;
   {
-    const Vec4<N> hm2 = seg_hraw<SEG>(xa2), hm1 = seg_hraw<SEG>(xa1);
-    gA = seg_hraw<SEG>(vert(hm2, hm1, hA, true));     // g[r0 - 1]
-    gB = seg_hraw<SEG>(vert(hm1, hA, hB, true));      // g[r0]
+    const Vec4<N> hm2 = seg_hraw<SEG>(xa2, L), hm1 = seg_hraw<SEG>(xa1, L);
+    gA = seg_hraw<SEG>(vert(hm2, hm1, hA, true), L);     // g[r0 - 1]
+    gB = seg_hraw<SEG>(vert(hm1, hA, hB, true), L);      // g[r0]
     if (top) gA = gB;
   }
   float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
   // z row i from the window; x = raw row i + 2
   auto row = [&](const Vec4<N>& x, const Vec4<N>& ha, const Vec4<N>& hb, Vec4<N>& hc, const Vec4<N>& ga,
                  const Vec4<N>& gb, Vec4<N>& gc, bool bottom_row) {
-    hc = seg_hraw<SEG>(x);
-    gc = seg_hraw<SEG>(vert(ha, hb, hc, true));
+    hc = seg_hraw<SEG>(x, L);
+    gc = seg_hraw<SEG>(vert(ha, hb, hc, true), L);
     if (bottom_row) gc = gb;
     seg_store<LAST>(L, ad, o_g, vert(ga, gb, gc, false));
     if (LAST) o_g += W;
@@ -685,9 +692,9 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLane
   else __syncwarp();
 }
 
-template <int SEG, bool CLEAN, int N, bool LAST>
-__device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, const SegLanes<N>& L, float* og, int H, int W,
-                                                 int c, float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
+template <int SEG, bool CLEAN, int N, bool LAST, bool E>
+__device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, const SegLanes<N, E>& L, float* og, int H,
+                                                 int W, int c, float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
   if (CLEAN) {
     switch (epi) {
       case 0: inplace_step_clean<SEG, N, LAST, 0>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
@@ -711,16 +718,20 @@ __device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, const S
 __host__ __device__ constexpr int inplace_warps_of(int nseg) { return nseg == 2 ? 8 : kInplaceWarps; }
 __host__ __device__ inline int inplace_nseg(int W) { return W > 128 ? 2 : 1; }
 
-// Whether seq_inplace takes the clean step (inplace_step_clean) for these planes.
-__host__ __device__ inline bool inplace_clean(int seg, int tile_planes, int H, int W) {
-  if (inplace_nseg(W) == 2) return true;   // planned only when clean (bs_api.cpp inplace_smem)
+// Which step seq_inplace runs for these planes: 0 = the one-step kernel (inplace_step: parts of
+// unequal height, or < 2 rows), 1 = clean steps with -inf pad lanes, 2 = clean steps with edge
+// selects (rows that fill their lane segment: W = 60, 64 with 16-lane segments).
+__host__ __device__ inline int inplace_mode(int seg, int tile_planes, int H, int W) {
+  if (inplace_nseg(W) == 2) return 1;   // planned only when clean (bs_api.cpp inplace_smem)
   const int parts = (kInplaceWarps / tile_planes) * (32 / seg);
-  return W / 4 + 2 <= seg && H % parts == 0 && H / parts >= 2;
+  if (H % parts != 0 || H / parts < 2) return 0;
+  return W / 4 + 2 <= seg ? 1 : 2;
 }
 
-template <int SEG, bool CLEAN, int NSEG>
+template <int SEG, int MODE, int NSEG>
 __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ? 1 : 4) seq_inplace(SeqArgs a) {
   constexpr int WARPS = inplace_warps_of(NSEG);
+  constexpr bool CLEAN = MODE != 0, EDGE = MODE == 2;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ int8_t epi_tab[kMaxSeqSteps];
   __shared__ const float2* aff_tab[kMaxSeqSteps];
@@ -785,7 +796,7 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
   const int cw = warp - 1;
   const int wpp = WARPS / a.tile_planes;
   const int sl = lane & (SEG - 1), half = lane / SEG;
-  const int c = 4 * (CLEAN ? sl - 1 : sl);            // clean: lane 0 of a segment is a -inf pad / halo
+  const int c = 4 * (MODE == 1 ? sl - 1 : sl);        // -inf pads: lane 0 of a segment is a pad / halo
   const int part = (cw % wpp) * (32 / SEG) + half;
   const int n_parts = wpp * (32 / SEG);
   const int Hp = (H + n_parts - 1) / n_parts;
@@ -812,7 +823,7 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
     float* og = a.out + (int64_t)plane * HW + c;
     // this lane's segments: pad lanes (outside the plane) read -inf and never store; halo lanes
     // (the neighbouring segment's edge group) read and never store
-    SegLanes<NSEG> L;
+    SegLanes<NSEG, EDGE> L;
 #pragma unroll
     for (int q = 0; q < NSEG; ++q) {
       const int cq = c + 4 * q * GS;                    // this lane's column in segment q
@@ -820,6 +831,8 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
       L.col_ok[q] = cq >= 0 && cq < W;
       L.st_ok[q] = p < np && L.col_ok[q] && (NSEG == 1 || (sl >= 1 && sl <= GS));
       L.ld[q] = PadLd{L.col_ok[q] ? ~0u : 127u, L.col_ok[q] ? 0u : smem_u32(s_ninf)};
+      L.le[q] = cq == 0;
+      L.re[q] = cq + 4 >= W;
     }
     int st = 0;
     if (CLEAN) {   // steps two at a time (one sweep per pair), an odd last step alone
@@ -851,10 +864,14 @@ size_t seq_inplace_smem(const SeqArgs& a) {
 }
 
 static const void* seq_fn(const SeqArgs& a) {
-  if (a.inplace_seg && inplace_nseg(a.W0) == 2) return (const void*)seq_inplace<32, true, 2>;
-  const bool clean = a.inplace_seg && inplace_clean(a.inplace_seg, a.tile_planes, a.H0, a.W0);
-  if (a.inplace_seg == 16) return clean ? (const void*)seq_inplace<16, true, 1> : (const void*)seq_inplace<16, false, 1>;
-  if (a.inplace_seg == 32) return clean ? (const void*)seq_inplace<32, true, 1> : (const void*)seq_inplace<32, false, 1>;
+  if (a.inplace_seg && inplace_nseg(a.W0) == 2) return (const void*)seq_inplace<32, 1, 2>;
+  const int mode = a.inplace_seg ? inplace_mode(a.inplace_seg, a.tile_planes, a.H0, a.W0) : 0;
+  if (a.inplace_seg == 16)
+    return mode == 1 ? (const void*)seq_inplace<16, 1, 1> : mode == 2 ? (const void*)seq_inplace<16, 2, 1>
+                                                                        : (const void*)seq_inplace<16, 0, 1>;
+  if (a.inplace_seg == 32)
+    return mode == 1 ? (const void*)seq_inplace<32, 1, 1> : mode == 2 ? (const void*)seq_inplace<32, 2, 1>
+                                                                        : (const void*)seq_inplace<32, 0, 1>;
   return (const void*)seq_staged;
 }
 

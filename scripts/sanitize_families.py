@@ -51,8 +51,11 @@ FAMILIES = [
     # planes 129..224 wide: one plane per CTA, two column segments per row with halo lanes
     ("seq_inplace_2seg", synth.synthetic51(3, batch=2, C=C, H=16).layers, (2, C, 16, 160), None,
      "sequence_staged_tma"),
-    # rows of 16 lane groups fill a 16-lane segment: the edge-select (not the -inf pad) in-place step
-    ("seq_inplace_edge", synth.synthetic51(3, batch=8, C=C, H=23).layers, (8, C, 23, 64), None,
+    # rows of 16 lane groups fill a 16-lane segment: edge selects instead of -inf pads -- two-step
+    # sweeps (equal row parts) and the one-step kernel (odd height: unequal parts)
+    ("seq_inplace_edge", synth.synthetic51(3, batch=8, C=C, H=24).layers, (8, C, 24, 64), None,
+     "sequence_staged_tma"),
+    ("seq_inplace_onestep", synth.synthetic51(3, batch=8, C=C, H=23).layers, (8, C, 23, 64), None,
      "sequence_staged_tma"),
     ("seq_halo", synth.synthetic51(5, batch=2, C=C, H=64).layers, (2, C, 64, 64), {"force_rows_per_task": 7},
      "sequence_staged_tma"),

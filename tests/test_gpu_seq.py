@@ -163,3 +163,33 @@ def test_inplace_wide_planes(H, W, cuda_dev, oracle_lib):
         U.assert_close(got, oracle.run_bf(layers, x), f"H={H} W={W} extra={extra}")
         other, _ = run_gpu(layers, x, {"force_tile_planes": 1})
         U.assert_bitexact(got, other, f"H={H} W={W} in-place vs shared tile / halo")
+
+
+@pytest.mark.parametrize("trial", range(48))
+def test_random_fast_sequences(trial, cuda_dev, oracle_lib):
+    """Random sequences of §5.1-type steps (3x3/s1/p1 max + any of BN (signed gamma) / ReLU / none)
+    on random planes (W a multiple of 4 up to 224, H 1..70 or up to 224): every sequence kernel the
+    planner picks (in place: clean two-step sweeps, single steps, edge selects, one or two column
+    segments; shared tile; halo) against the oracle, and bit for bit against the shared-tile / halo
+    kernels (force_tile_planes)."""
+    import random
+    rng = random.Random(900 + trial)
+    W = 4 * rng.randint(1, 56)
+    H = rng.randint(1, 70) if rng.random() < 0.7 else 8 * rng.randint(2, 28)
+    C = rng.randint(1, 5)
+    N = rng.randint(1, 3) if H * W < 20000 else 1
+    layers = []
+    for b in range(rng.randint(1, 9)):
+        layers.append(synth.maxpool(3, 1, 1))
+        r = rng.random()
+        if r < 0.6:
+            layers.append(synth.batchnorm(C, 50 + b, signed_gamma=rng.random() < 0.5))
+        if rng.random() < 0.6:
+            layers.append(synth.relu())
+    shape = (N, C, H, W)
+    x = synth.uniform_np(7000 + trial, int(np.prod(shape))).reshape(shape)
+    got, plan = run_gpu(layers, x)
+    ctx = f"trial {trial} shape {shape} {len(layers)} layers {_bs().bs_plan_query_launch(plan, 0)}"
+    U.assert_close(got, oracle.run_bf(layers, x), ctx)
+    other, _ = run_gpu(layers, x, {"force_tile_planes": 1})
+    U.assert_bitexact(got, other, ctx + " vs shared tile / halo")
