@@ -25,6 +25,7 @@ timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $O/bench_ref
 fi
 if [ -z "$NOSEC" ]; then
 timeout 900 python scripts/exp_sec51.py $O/sec51_56.jsonl 128 64 56 1,2,4,8,12,16,17,20,24,32,40 > /dev/null 2> $O/sec51_56.err
+timeout 900 python scripts/exp_sec51.py $O/sec51_64.jsonl 128 64 64 1,16,40 --no-eager > /dev/null 2> $O/sec51_64.err
 timeout 900 python scripts/exp_sec51.py $O/sec51_112.jsonl 64 64 112 1,5,16,32,40 --no-eager > /dev/null 2> $O/sec51_112.err
 timeout 900 python scripts/exp_sec51.py $O/sec51_224.jsonl 32 64 224 1,5,8,15,16,30,40 --no-eager > /dev/null 2> $O/sec51_224.err
 # the paper's cache-limit artifact: 224^2 planes under a 110 KB budget -> halo tiles

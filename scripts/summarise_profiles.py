@@ -160,7 +160,7 @@ with open(os.path.join(DST, "ncu_full_summary.md"), "w") as fo:
                  f"{d['traffic_over_alg']:.3f} | {d['alg_gbs_under_ncu']:.0f} | {int(d.get('regs', 0))} | "
                  f"{d.get('warps_per_sm', 0):.1f} | {d.get('issue_active_pct', 0):.0f} | "
                  f"{', '.join(f'{k} {v}%' for k, v in d['top_stalls'].items())} |\n")
-for f in ("bench_default.json", "bench_2rank_gloo.json", "bench_reference.json", "sec51_56.jsonl", "sec51_112.jsonl",
+for f in ("bench_default.json", "bench_2rank_gloo.json", "bench_reference.json", "sec51_56.jsonl", "sec51_64.jsonl", "sec51_112.jsonl",
           "sec51_224.jsonl", "sec51_224_budget110k.jsonl", "pytest_gpu.log", "smoke.log", "gpu.txt", "nproc.txt", "sanitize_rc.txt"):
     if os.path.exists(os.path.join(SRC, f)):
         shutil.copy(os.path.join(SRC, f), os.path.join(DST, f))
