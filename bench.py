@@ -731,6 +731,19 @@ def measure_lbl(ctx, m):
             "what": "torch eager F.batch_norm/relu/max_pool2d/avg_pool2d, one kernel per layer, same GPU"}
 
 
+def attach_ceiling(m, stacks):
+    """The dominant kernel's time against the same-size ideal streaming kernel (per_stack): a
+    fraction <= ~1 beside roofline.frac, whose copy-bandwidth peak a 4:1 read-dominated stream can
+    exceed."""
+    if not stacks:
+        return
+    for st in stacks:
+        if st["stack"] == m["roofline"].get("stack"):
+            m["roofline"]["frac_of_ceiling"] = st["frac_of_ceiling"]
+            m["roofline"]["ceiling_gbs"] = st["gbs"] / st["frac_of_ceiling"] if st["frac_of_ceiling"] else None
+            m["roofline"]["ceiling_variant"] = st["ceiling_variant"]
+
+
 def per_stack(ctx, m):
     I = m["_internal"]
     return [measure_stack_alone(ctx, c, I["plans"][c.name], I["infos"][c.name]) for c in I["cases"]]
@@ -793,6 +806,7 @@ def main():
     e2e = measure_e2e(ctx, m)
     lbl = measure_lbl(ctx, m) if (not args.no_lbl and ctx.rank == 0) else None
     stacks = per_stack(ctx, m) if do_stacks else None
+    attach_ceiling(m, stacks)
     cpu = None
     if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
         v, n, T = time_oracle(m["_internal"]["cases"], args.cpu_budget, 1 << 20)
@@ -814,6 +828,7 @@ def main():
             mw = measure(ctx, wl, full=False)
             if do_stacks:
                 mw["per_stack"] = per_stack(ctx, mw)
+                attach_ceiling(mw, mw["per_stack"])
             del mw["_internal"]
             extras[wl] = mw
         extras["c1"] = measure_c1(ctx)
