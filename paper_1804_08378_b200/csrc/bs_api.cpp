@@ -608,10 +608,10 @@ int64_t inplace_smem(const std::vector<Step>& steps, size_t a, size_t b, const b
   if (W > 224) return -1;
   for (size_t k = a; k < b; ++k)
     if (!is_fast_step(steps[k]) || steps[k].in.w != W || steps[k].in.h != H) return -1;
-  // planes 129..224 wide: one plane per CTA, 8 warps each owning H / 8 rows of both column
-  // segments of the row (k_seq.cu seq_inplace<32, true, 2>); only with equal parts of >= 2 rows
+  // planes 129..224 wide: one plane per CTA, 8 warps each owning ~H / 8 rows of both column
+  // segments of the row (k_seq.cu seq_inplace<32, 1, 2>); parts of >= 2 rows
   const bool wide = W > 128;
-  if (wide && (H % 8 != 0 || H < 16)) return -1;
+  if (wide && H < 16) return -1;
   const int64_t warps = wide ? 8 : kInplaceWarps;
   // planes per CTA: warps per plane chosen so that ~4 CTAs (16 consumer warps) fit an SM: small
   // planes one warp each, 112 x 112 planes four warps each

@@ -721,10 +721,13 @@ __host__ __device__ inline int inplace_nseg(int W) { return W > 128 ? 2 : 1; }
 // Which step seq_inplace runs for these planes: 0 = the one-step kernel (inplace_step: parts of
 // unequal height, or < 2 rows), 1 = clean steps with -inf pad lanes, 2 = clean steps with edge
 // selects (rows that fill their lane segment: W = 60, 64 with 16-lane segments).
+// Clean steps need >= 2 rows per part; the two half-warp parts of a 16-lane-segment warp walk in
+// lockstep, so there all parts must be equal; whole-warp parts (32-lane segments) may differ by a
+// row (balanced split).
 __host__ __device__ inline int inplace_mode(int seg, int tile_planes, int H, int W) {
   if (inplace_nseg(W) == 2) return 1;   // planned only when clean (bs_api.cpp inplace_smem)
   const int parts = (kInplaceWarps / tile_planes) * (32 / seg);
-  if (H % parts != 0 || H / parts < 2) return 0;
+  if (seg == 16 ? (H % parts != 0 || H / parts < 2) : H < 2 * parts) return 0;
   return W / 4 + 2 <= seg ? 1 : 2;
 }
 
@@ -799,7 +802,10 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
   const int c = 4 * (MODE == 1 ? sl - 1 : sl);        // -inf pads: lane 0 of a segment is a pad / halo
   const int part = (cw % wpp) * (32 / SEG) + half;
   const int n_parts = wpp * (32 / SEG);
-  const int Hp = (H + n_parts - 1) / n_parts;
+  const int Hp = (H + n_parts - 1) / n_parts;          // one-step kernel: equal parts (the last shorter)
+  // clean steps: balanced parts (equal whenever two parts share a warp, see inplace_mode)
+  const int c_r0 = CLEAN ? part * H / n_parts : part * Hp;
+  const int c_hp = CLEAN ? (part + 1) * H / n_parts - c_r0 : Hp;
   const int bar_id = wpp > 1 ? 1 + cw / wpp : 0;       // named barrier of the plane's warps
   float2* const t_aff = (float2*)(stage0 + (size_t)a.stages * a.stage_bytes) + (size_t)cw * n;   // this warp's
   // column segments: NSEG = 2 splits a row's W / 4 groups into two halves of GS groups
@@ -839,19 +845,19 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
       for (; st + 1 < n; st += 2) {
         const float lo1 = (epi_tab[st] & 1) ? 0.f : -CUDART_INF_F, lo2 = (epi_tab[st + 1] & 1) ? 0.f : -CUDART_INF_F;
         if (st + 2 == n)
-          inplace_pair_clean<SEG, NSEG, true>(base, L, og, H, W, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp, Hp,
+          inplace_pair_clean<SEG, NSEG, true>(base, L, og, H, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
                                               bar_id, 32 * wpp);
         else
-          inplace_pair_clean<SEG, NSEG, false>(base, L, og, H, W, t_aff[st], lo1, t_aff[st + 1], lo2, part * Hp, Hp,
+          inplace_pair_clean<SEG, NSEG, false>(base, L, og, H, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
                                                bar_id, 32 * wpp);
       }
     }
     for (; st < n; ++st) {
       const float2 aff = t_aff[st];
       if (st == n - 1)
-        inplace_step_epi<SEG, CLEAN, NSEG, true>(epi_tab[st], base, L, og, H, W, c, aff, part * Hp, Hp, bar_id, 32 * wpp);
+        inplace_step_epi<SEG, CLEAN, NSEG, true>(epi_tab[st], base, L, og, H, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp);
       else
-        inplace_step_epi<SEG, CLEAN, NSEG, false>(epi_tab[st], base, L, og, H, W, c, aff, part * Hp, Hp, bar_id, 32 * wpp);
+        inplace_step_epi<SEG, CLEAN, NSEG, false>(epi_tab[st], base, L, og, H, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp);
     }
     mbar_arrive(&empty[s]);   // every lane: the tile's stage is free for the producer
   }

@@ -143,10 +143,11 @@ def test_inplace_kernel_heights(H, cuda_dev, oracle_lib):
         U.assert_bitexact(got, other, f"H={H} W={W} in-place vs shared tile")
 
 
-@pytest.mark.parametrize("H,W", [(16, 132), (24, 200), (40, 160), (56, 224), (224, 224)])
+@pytest.mark.parametrize("H,W", [(16, 132), (24, 200), (40, 160), (56, 224), (224, 224), (30, 144), (51, 224)])
 def test_inplace_wide_planes(H, W, cuda_dev, oracle_lib):
-    """Planes 129..224 wide run in place too (k_seq.cu seq_inplace<32, true, 2>): one plane per CTA,
-    8 warps of H / 8 rows, each row as two column segments with halo lanes; even and odd step
+    """Planes 129..224 wide run in place too (k_seq.cu seq_inplace<32, 1, 2>): one plane per CTA,
+    8 warps of ~H / 8 rows (balanced, unequal when 8 does not divide H), each row as two column
+    segments with halo lanes; even and odd step
     counts (two-step sweeps + a single step), signed-gamma BN; bit for bit equal to the
     shared-tile / halo kernels (force_tile_planes routes there) and within tolerance of the oracle."""
     bs = _bs()
