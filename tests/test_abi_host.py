@@ -277,6 +277,20 @@ def test_graph_argument_errors(bs):
     bs._lib.bs_graph_destroy(None)                              # NULL-safe
 
 
+def test_execute_host_batch_argument_errors(bs):
+    """bs_execute_host_batch validates every execution like bs_execute_host, naming its index (no
+    GPU needed to fail): host_only plans, NULL arrays, a negative count; an empty batch is a no-op."""
+    import ctypes
+    good = host_plan(bs, [synth.relu()], (1, 2, 4, 4))
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_execute_host_batch([good], [[1 << 20]], [1 << 21], [[1 << 22]], [1 << 23], stream=0)
+    assert e.value.status == 2 and "execution 0" in str(e.value) and "host_only" in str(e.value)
+    bs.bs_execute_host_batch([], [], [], [], [], stream=0)       # nothing to do
+    assert bs._lib.bs_execute_host_batch(None, 1, None, None, None, None, None, 0, None) == 2
+    assert bs._lib.bs_execute_host_batch(None, -1, None, None, None, None, None, 0, None) == 2
+    assert bs._lib.bs_execute_host_batch(None, 0, None, None, None, None, None, 0, None) == 0
+
+
 def test_staged_ring_policy(bs):
     """Staged pools: tiles sized so the 8 consumer warps share each tile (<= 16 items), and the
     grid sized for ~104 KB of tiles in flight per SM -- one CTA per SM for >= 20 KB tiles with
