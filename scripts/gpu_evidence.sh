@@ -33,7 +33,7 @@ BS_SEC51_OPTS='{"smem_budget_bytes": 112640}' timeout 900 python scripts/exp_sec
 fi
 if [ -z "$NONCU" ]; then
 # launch list of a short default bench (cold-cache, serialised: compare shares)
-$NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+[ -z "$NOFULL" ] && $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
      --log-file $O/launches_resnet50.csv python bench.py --steps 2 --warmup 3 --no-extra --no-lbl --no-per-stack \
      --no-cpu-baseline --no-validate --e2e-steps 1 > $O/launches_resnet50.log 2>&1
 # DRAM traffic per launch of each workload's dominant stack (cold cache)
@@ -42,6 +42,7 @@ for spec in "resnet50 0" "alexnet 0" "vgg16 0" "densenet121 11"; do
   $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
        --log-file $O/traffic_$1_$2.csv python scripts/prof_one.py $1 $2 3 > $O/traffic_$1_$2.log 2>&1
 done
+[ -n "$NOFULL" ] && { du -sh $O; exit 0; }   # (NOFULL=1: the traffic captures only)
 for spec in "resnet50 0 pool_vec" "alexnet 0 pool_staged" "densenet121 11 ew_kernel" "densenet121 -1 pool_planes"; do
   set -- $spec
   $NCU --set full --clock-control none --import-source on -k regex:$3 -s 1 -c 1 -o /tmp/full_$1_$2 -f \

@@ -102,7 +102,8 @@ for f in sorted(glob.glob(os.path.join(SRC, "full_*.raw.csv"))):
             d["thread_instructions_per_output"] = 32 * d.get("warp_instructions", 0) / outs
         summary.append(d)
     shutil.copy(f.replace(".raw.csv", ".details.csv"), os.path.join(DST, os.path.basename(f).replace(".raw.csv", ".details.csv")))
-json.dump(summary, open(os.path.join(DST, "ncu_full_summary.json"), "w"), indent=1)
+if summary:
+    json.dump(summary, open(os.path.join(DST, "ncu_full_summary.json"), "w"), indent=1)
 
 # ---- DRAM traffic of each workload's dominant stack (cold cache), keyed by kernel-source hash
 traffic = {"sources_sha16": bench.kernel_sources_hash(), "captured": tag,
@@ -145,7 +146,7 @@ if os.path.exists(lp):
         for st, (n, t, b, kn) in per.items():
             fo.write(f"{st:26s} {kn[:28]:28s} {n:8d} {t * 1e6 / n:8.1f} {100 * t / tot:6.1f}% {b / n / 1e6:15.1f}\n")
 
-with open(os.path.join(DST, "ncu_full_summary.md"), "w") as fo:
+with open(os.path.join(DST, "ncu_full_summary.md") if summary else os.devnull, "w") as fo:
     fo.write(f"# {tag}: ncu --set full, one launch of each captured kernel\n\n")
     fo.write("`scripts/gpu_evidence.sh` (`ncu --set full --clock-control none --import-source on`, 1 launch after 1\n"
              "warm-up launch).  traffic/alg = DRAM bytes read+written / algorithmic bytes (one read of the input +\n"
@@ -166,7 +167,8 @@ for f in ("bench_default.json", "bench_2rank_gloo.json", "bench_reference.json",
         shutil.copy(os.path.join(SRC, f), os.path.join(DST, f))
 for f in glob.glob(os.path.join(SRC, "sanitize_*.log")):
     shutil.copy(f, os.path.join(DST, os.path.basename(f)))
-print(open(os.path.join(DST, "ncu_full_summary.md")).read())
+if summary:
+    print(open(os.path.join(DST, "ncu_full_summary.md")).read())
 if os.path.exists(os.path.join(DST, "ncu_launches_resnet50.txt")):
     print(open(os.path.join(DST, "ncu_launches_resnet50.txt")).read())
 print(json.dumps(traffic, indent=1))
