@@ -68,11 +68,16 @@ def instances(cases):
 
 
 def kernel_sources_hash() -> str:
-    """sha256 (16 hex) of the kernel + planner sources: keys stored ncu traffic to the build."""
+    """sha256 (16 hex) of the kernel + planner sources with comments and blank lines removed: keys
+    stored ncu traffic to the code that was profiled (a comment edit does not invalidate it)."""
     import glob
+    import re
     h = hashlib.sha256()
     for p in sorted(glob.glob(os.path.join(ROOT, "paper_1804_08378_b200", "csrc", "*"))):
-        h.update(open(p, "rb").read())
+        text = open(p, encoding="utf-8").read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        lines = [re.sub(r"//.*$", "", ln).rstrip() for ln in text.splitlines()]
+        h.update("\n".join(ln for ln in lines if ln.strip()).encode())
     return h.hexdigest()[:16]
 
 

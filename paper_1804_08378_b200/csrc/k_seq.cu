@@ -7,10 +7,13 @@ namespace bs {
 //
 // NEXT-2: a *sequence* of several steps runs on-chip (PAPER.md P:L545-558,
 // lst:finalcode P:L512-530 "float cached_data[...]"; the paper's GPU kernel swapped two smem
-// buffers per step).  A tile is bulk-copied (TMA, cp.async.bulk) into a ring stage;
-// step 0 reads the stage, every later step reads the previous step's work buffer (two ping-pong
-// buffers in shared memory), and only the last step writes HBM.  A named barrier over the 8
-// consumer warps separates steps.
+// buffers per step).  Two kernels:
+//  * seq_inplace (below; the planner's choice for §5.1-type sequences on whole planes <= 224
+//    wide): warp groups own planes for the whole sequence and sweep them in place, two steps per
+//    sweep;
+//  * seq_staged (this section; every other sequence): a tile is bulk-copied (TMA,
+//    cp.async.bulk) into a ring stage; its steps ping-pong between the stage and ONE work buffer,
+//    and only the last step writes HBM.  A named barrier over the 8 consumer warps separates steps.
 //
 // Tiles (chosen by the planner, bs_api.cpp plan_sequence):
 //  * whole planes: P planes per tile, no halo at all;
@@ -363,18 +366,22 @@ __global__ void __launch_bounds__(kSeqThreads) seq_staged(SeqArgs a) {
 
 // ------------------------------------------------------------------ in-place, warp per plane
 //
-// Sequences made only of fast steps (the §5.1 block) on whole planes of W <= 128: one or a few
+// Sequences made only of fast steps (the §5.1 block) on whole planes (W <= 224): one or a few
 // consumer warps own a plane of the tile for the WHOLE sequence, so steps need no CTA barrier and
-// no work buffer.  The plane's rows are cut into parts, one per half-warp (16-lane segments, W <= 64)
-// or warp; parts of one plane in different warps meet at a named barrier twice per step (after each
-// part has read its neighbours' boundary rows, and at the end).  A step runs down a part's rows in place: output row i is written over input row i after
-// input row i+1 has been loaded, and the rows above are only needed as horizontal maxima already
-// held in registers; a lane loads and stores only its own 4 columns (neighbour columns arrive by
-// shuffle from the same load), so nothing is overwritten before it is read.  The one exception is
-// the row just below a part, which the next part overwrites first: it is read once, before any
-// part writes.  The next input row is loaded one
-// iteration ahead.  Shared memory per tile is the stage alone, so many CTAs share an SM and the bulk
-// copy of one CTA's next tile overlaps the other CTAs' steps.
+// no work buffer.  The plane's rows are cut into parts, one per half-warp (16-lane segments,
+// W <= 64) or warp; parts of one plane in different warps meet at a named barrier twice per sweep
+// (after each part has read its neighbours' boundary rows, and at the end).  A sweep runs down a
+// part's rows in place: output row i is written over input row i after the rows below it that
+// its window needs have been loaded, and the rows above are only needed as horizontal maxima
+// already held in registers; a lane loads and stores only its own columns (neighbour columns
+// arrive by shuffle from the same load), so nothing is overwritten before it is read.  The
+// exceptions are the rows just outside a part, which a neighbouring part overwrites: they are read
+// once, before any part writes.  Loads run one row ahead.  Shared memory per tile is the stage
+// alone, so several CTAs share an SM and the bulk copy of one CTA's next tile overlaps the other
+// CTAs' steps (planes 129..224 wide: one plane per CTA).  Three step kernels below: the one-step
+// sweep with edge selects (inplace_step, any part heights), and the clean one-step and two-step
+// sweeps (inplace_step_clean, inplace_pair_clean: -inf pad lanes or edge selects, 1 or 2 column
+// segments).
 // One in-place step of one row part [r0, r0 + Hp) of a plane (Hp rows per part; the last part may
 // have fewer).  bar_id > 0: the plane's parts live in several warps (named barrier over them).
 template <int SEG, bool LAST, int EPI>
