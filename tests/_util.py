@@ -151,3 +151,28 @@ def make_inputs(layers, shape, n_ops, seed, shapes):
             ops[L.operand - 1] = synth.uniform_np(seed + 7919 * L.operand,
                                                   int(np.prod(s))).reshape(s)
     return x, ops
+
+
+def torch_definition(layers, x, ops=()):
+    """The breadth-first definition (R1: each layer in fp64, rounded once to fp32 when stored)
+    written with torch library ops on the GPU -- an independent check of EVERY element at full
+    size (the oracle checks sampled images one by one above)."""
+    import torch
+    import torch.nn.functional as F
+    t = x.double()
+    for L in layers:
+        if L.kind == "batchnorm":
+            f = lambda a: torch.from_numpy(np.asarray(a, np.float64)).to(x.device).view(1, -1, 1, 1)
+            t = (t - f(L.mean)) / torch.sqrt(f(L.var) + float(np.float32(L.eps))) * f(L.gamma) + f(L.beta)
+        elif L.kind == "relu":
+            t = torch.clamp_min(t, 0.0)
+        elif L.kind == "maxpool":
+            t = F.max_pool2d(t, L.kernel, L.stride, L.padding)
+        elif L.kind == "avgpool":
+            t = F.avg_pool2d(t, L.kernel, L.stride, L.padding, count_include_pad=L.count_include_pad)
+        elif L.kind == "scale":
+            t = t * float(L.alpha)
+        elif L.kind == "add":
+            t = t + ops[L.operand - 1].double()
+        t = t.float().double()                      # stored as fp32 between layers
+    return t.float()

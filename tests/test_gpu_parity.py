@@ -92,30 +92,6 @@ def test_full_size_sampled(wl, cuda_dev, oracle_lib):
         del x, out
 
 
-def _torch_definition(layers, x, ops):
-    """The breadth-first definition (R1: each layer in fp64, rounded once to fp32 when stored)
-    written with torch library ops on the GPU -- an independent check of EVERY element at full
-    size (the oracle checks sampled images one by one above)."""
-    import torch.nn.functional as F
-    t = x.double()
-    for L in layers:
-        if L.kind == "batchnorm":
-            f = lambda a: torch.from_numpy(np.asarray(a, np.float64)).to(x.device).view(1, -1, 1, 1)
-            t = (t - f(L.mean)) / torch.sqrt(f(L.var) + float(np.float32(L.eps))) * f(L.gamma) + f(L.beta)
-        elif L.kind == "relu":
-            t = torch.clamp_min(t, 0.0)
-        elif L.kind == "maxpool":
-            t = F.max_pool2d(t, L.kernel, L.stride, L.padding)
-        elif L.kind == "avgpool":
-            t = F.avg_pool2d(t, L.kernel, L.stride, L.padding, count_include_pad=L.count_include_pad)
-        elif L.kind == "scale":
-            t = t * float(L.alpha)
-        elif L.kind == "add":
-            t = t + ops[L.operand - 1].double()
-        t = t.float().double()                      # stored as fp32 between layers
-    return t.float()
-
-
 @pytest.mark.parametrize("wl", ["alexnet", "vgg16", "resnet50", "densenet121", "resnet50_residual"])
 def test_full_size_every_element(wl, cuda_dev):
     """Every stack of every BASELINE.json config at its full batch, in bench.py's launch
@@ -133,7 +109,7 @@ def test_full_size_every_element(wl, cuda_dev):
         plan = bs.bs_plan_create(case.layers, case.shape)
         out = torch.empty(bs.bs_plan_query(plan)["out"], device="cuda")
         bs.bs_execute_ex(plan, [x] + ops, out)
-        ref = _torch_definition(case.layers, x, ops)
+        ref = U.torch_definition(case.layers, x, ops)
         torch.cuda.synchronize()
         if U.needs_tolerance(case.layers):
             err = (out.double() - ref.double()).abs() - (1e-6 + 1e-5 * ref.double().abs())

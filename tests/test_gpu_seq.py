@@ -116,6 +116,10 @@ def test_sec51_full_shapes_sampled(shape, depth, cuda_dev, oracle_lib):
     for n in (0, shape[0] - 1):
         ref = oracle.run_bf(case.layers, x[n:n + 1].cpu().numpy())
         U.check(out[n:n + 1].cpu().numpy(), ref, case.layers, f"{shape} image {n}")
+    # every element against the definition written with torch library ops (fp64 per layer)
+    ref = U.torch_definition(case.layers, x)
+    err = (out.double() - ref.double()).abs() - (1e-6 + 1e-5 * ref.double().abs())
+    assert float(err.max()) <= 0, f"{shape}: max excess {float(err.max())}"
 
 
 @pytest.mark.parametrize("H", [1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 23, 56, 112])
