@@ -593,6 +593,10 @@ def stored_traffic(wl, stack, alg_bytes):
     if tr.get("sources_sha16") != kernel_sources_hash():
         out["traffic_source"] = f"stale: {p} was captured from kernel sources {tr.get('sources_sha16')}"
         return out
+    if e.get("alg_bytes_per_launch") != alg_bytes:   # another batch (e.g. a strong-scaled shard)
+        out["traffic_source"] = (f"not comparable: captured at {e.get('alg_bytes_per_launch')} algorithmic bytes "
+                                 f"per launch, this launch moves {alg_bytes}")
+        return out
     out["traffic"] = e["dram_bytes_per_launch"]
     out["traffic_ratio_to_alg"] = e["dram_bytes_per_launch"] / alg_bytes
     out["traffic_source"] = f"ncu --set full, {tr.get('captured')} ({os.path.relpath(p, ROOT)})"
@@ -600,8 +604,9 @@ def stored_traffic(wl, stack, alg_bytes):
 
 
 def measure_e2e(ctx, m):
-    """End to end through bs_execute_host: every step copies each stack's inputs from pinned host
-    memory, runs the kernels and copies the outputs back (pipelined per image chunk)."""
+    """End to end through bs_execute_host_batch: every step copies each stack's inputs from pinned
+    host memory, runs the kernels and copies the outputs back (pipelined per image chunk and across
+    the step's stacks)."""
     torch, bs, args = ctx.torch, ctx.bs, ctx.args
     I = m["_internal"]
     cases, infos, inst, bufs, n_sets, handles = I["cases"], I["infos"], I["inst"], I["bufs"], I["n_sets"], I["handles"]
