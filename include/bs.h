@@ -223,7 +223,7 @@ BS_API bs_status bs_execute_ex(const bs_plan *plan, const float *const *inputs, 
  *   d_inputs[n_inputs], d_out : caller-owned device buffers of the same shapes (staging).
  *   n_chunks           : the batch is split into n_chunks image ranges; chunk k's
  *                        host->device copy, kernels, and device->host copy are pipelined
- *                        across the plan's two copy streams and `stream` (0 = 8 chunks;
+ *                        across the plan's two copy streams and `stream` (0 = 4 chunks;
  *                        at most one chunk per image).
  * Returns after ENQUEUEING; the caller synchronises `stream` before reading h_out.
  */

@@ -1173,9 +1173,9 @@ bs_status pipeline_host(const bs_plan* plan, const float* const* h_inputs, int32
                         float* const* d_inputs, float* d_out, int32_t n_chunks, cudaStream_t cs, cudaStream_t h2d,
                         cudaStream_t d2h, cudaEvent_t copied, cudaEvent_t done) {
   const int64_t N = plan->launches.front().step.in.n;
-  // default: 8 chunks (measured on the ResNet-50 step: 2, 8, ~8 MB per chunk and 31 chunks are
-  // within noise of each other and of plain pinned copies of the same bytes -- PCIe-bound)
-  if (n_chunks <= 0) n_chunks = 8;
+  // default: 4 chunks (ResNet-50 step through bs_execute_host_batch, images/s: 1 chunk 2872,
+  // 2: 2963, 4: 2995, 8: ~2930, 16: 2755 -- few large copies, and enough to overlap within a stack)
+  if (n_chunks <= 0) n_chunks = 4;
   n_chunks = (int32_t)std::min<int64_t>(n_chunks, N);
   // per-image byte sizes of each input and the output
   std::vector<int64_t> in_img(n_inputs);
