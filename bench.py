@@ -780,6 +780,34 @@ def measure_c1(ctx):
     return out
 
 
+def measure_sec51(ctx):
+    """PAPER.md §5.1 (NEXT-2): the synthetic network of MaxPool3x3/s1/p1 -> BN -> ReLU blocks on
+    (128, 64, 56, 56) as one on-chip sequence (the planner) against one step per sequence (one HBM
+    round trip per block), R back-to-back executions over rotating buffers in one CUDA graph."""
+    bs = ctx.bs
+    out = {"what": "PAPER.md §5.1 blocks MaxPool3x3/s1/p1 -> BN -> ReLU on (128, 64, 56, 56), us per block",
+           "rows": []}
+    for depth in (16, 40):
+        case = synth.synthetic51(depth)
+        row = {"depth": depth}
+        for policy, name in ((1, "one_step_per_sequence"), (0, "planner")):
+            plan = bs.bs_plan_create(case.layers, case.shape, {"max_steps_per_sequence": policy})
+            info = bs.bs_plan_query(plan)
+            sb, R = stack_burst(ctx, case, plan, info["alg_bytes_read"] + info["alg_bytes_written"], 29)
+
+            def burst():
+                for r in range(R):
+                    xs, y = sb[r % len(sb)]
+                    ctx.launch(plan, xs, y)
+            ms = ctx.burst_ms(burst) / R
+            row[name] = {"us_per_block": 1e3 * ms / depth, "sequences": info["n_sequences"],
+                         "kernel": bs.KERNEL_NAMES[bs.bs_plan_query_launch(plan, 0)["kernel"]]}
+            del sb, plan
+        row["speedup"] = row["one_step_per_sequence"]["us_per_block"] / row["planner"]["us_per_block"]
+        out["rows"].append(row)
+    return out
+
+
 def strip(m):
     return {k: v for k, v in m.items() if not k.startswith("_")}
 
@@ -842,6 +870,7 @@ def main():
             del mw["_internal"]
             extras[wl] = mw
         extras["c1"] = measure_c1(ctx)
+        extras["sec51"] = measure_sec51(ctx)
 
     if ctx.rank == 0:
         line = {
