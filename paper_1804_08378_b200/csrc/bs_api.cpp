@@ -740,6 +740,50 @@ void plan_sequence(const bs_plan* p, const std::vector<Step>& steps, size_t a, s
   l.seq_in_pitch = g.in_pitch;
   l.seq_out_pitch = g.out_pitch;
   l.seq_ranges = g.ranges;
+  // Halo tiles of §5.1-type sequences run in place (k_seq.cu seq_inplace, band tiles): the same
+  // bands and split points as the shared-tile kernel (the paper's footprint rule, R14/R15), but a
+  // band is swept in place with two steps per sweep -- its stage alone, no work buffer.  Planner-
+  // chosen bands only (forced bands keep testing seq_staged), whole-warp row parts (W > 56) of
+  // >= 2 rows each.
+  const int64_t W = steps[a].in.w;
+  bool band_inplace = g.n_bands > 1 && o.force_rows_per_task <= 0 && o.force_tile_planes <= 0 && W > 56 && W <= 224;
+  for (size_t k = a; k < b && band_inplace; ++k) band_inplace = is_fast_step(steps[k]) && steps[k].in.w == W;
+  if (band_inplace) {
+    const int64_t parts = W > 128 ? 8 : kInplaceWarps;
+    // the in-place footprint is the band alone (2 stages, no work buffer): the tallest band whose
+    // two stages fit the budget, then balanced (no short last band); the seq_staged geometry in
+    // `l` stays untouched unless every band qualifies
+    int64_t halo = 0;   // input rows beyond a band's output rows (both sides, interior band)
+    for (size_t k = a; k < b; ++k) halo += 2 * steps[k].ph;
+    const int64_t cap_rows = (seq_band_cap(o) - 4096 - (int64_t)(b - a) * 8 * 8) / (2 * (W * 4 + 1));
+    const int64_t Rmax = std::max<int64_t>(g.R, std::min<int64_t>(Ho, cap_rows - halo));
+    const int64_t nb = (Ho + Rmax - 1) / Rmax, Rb = (Ho + nb - 1) / nb;
+    SeqGeom gb = g;
+    if (Rb != g.R) {
+      seq_geometry(steps, a, b, 1, Rb, 2, gb);
+      seq_chunking(steps, a, b, gb);
+    }
+    int64_t max_rows = 0;
+    for (int64_t bd = 0; bd < gb.n_bands; ++bd) {
+      const SeqRange& r0 = gb.ranges[(size_t)bd * (b - a)];
+      band_inplace = band_inplace && r0.in_hi - r0.in_lo >= 2 * parts;
+      max_rows = std::max<int64_t>(max_rows, r0.in_hi - r0.in_lo);
+    }
+    if (band_inplace) {
+      l.seq_bands = (int32_t)gb.n_bands;
+      l.seq_band_rows = (int32_t)gb.R;
+      l.seq_in_pitch = gb.in_pitch;
+      l.seq_out_pitch = gb.out_pitch;
+      l.seq_ranges = gb.ranges;
+      l.seq_inplace_seg = 32;
+      l.tile_planes = 1;
+      l.seq_work_floats = 0;
+      l.seq_stage_bytes = (int32_t)((max_rows * W * 4 + 16 + 127) / 128 * 128);
+      // two stages when they fit the budget: band tiles are short, and the two-segment kernel runs
+      // one CTA per SM (registers), so the next band's copy must overlap this band's sweeps
+      l.stages = 2 * (int64_t)l.seq_stage_bytes + 4096 <= seq_band_cap(o) ? 2 : 1;
+    }
+  }
 }
 
 void pack_and_tile(bs_plan* p, std::vector<Step>& steps, const bs_plan_options& o) {

@@ -524,7 +524,8 @@ __device__ __forceinline__ void seg_store(const SegLanes<N, E>& L, uint32_t ad, 
 
 template <int SEG, int N, bool LAST, int EPI, bool E>
 __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLanes<N, E>& L, float* og, int H, int W,
-                                                   float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
+                                                   float2 aff, int r0, int Hp, int bar_id, int bar_threads, int slo,
+                                                   int shi) {
   const uint32_t W4 = 4u * (uint32_t)W;
   auto epi = [&](float v) -> float {
     if (EPI >= 2) v = __fmaf_rn(v, aff.x, aff.y);
@@ -540,6 +541,7 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
   if (bar_id) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
   else __syncwarp();                                 // the other half-warp's part
   float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
+  int orow = r0;                                      // the row being output (the last step stores [slo, shi))
   Vec4<N> hC;
   auto out = [&](const Vec4<N>& a, const Vec4<N>& b, const Vec4<N>& c) {
     Vec4<N> o;
@@ -550,8 +552,8 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
       o.s[q].z = epi(max3f(a.s[q].z, b.s[q].z, c.s[q].z));
       o.s[q].w = epi(max3f(a.s[q].w, b.s[q].w, c.s[q].w));
     }
-    seg_store<LAST>(L, ad, o_g, o);
-    if (LAST) o_g += W;
+    if (!LAST || (orow >= slo && orow < shi)) seg_store<LAST>(L, ad, o_g, o);
+    if (LAST) { o_g += W; ++orow; }
     ad += W4;
   };
   // output row i (i + 2 < Hp): raw row i + 2 is loaded before row i is overwritten
@@ -604,7 +606,7 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
 template <int SEG, int N, bool LAST, bool E>
 __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLanes<N, E>& L, float* og, int H, int W,
                                                    float2 a1, float lo1, float2 a2, float lo2, int r0, int Hp,
-                                                   int bar_id, int bar_threads) {
+                                                   int bar_id, int bar_threads, int slo, int shi) {
   const uint32_t W4 = 4u * (uint32_t)W;
   // A pad lane's step-k row must stay -inf (its neighbours take it as their outer column), but its
   // horizontal maxima pick up the edge columns through the shuffles: (s, t) = (0, -inf) maps any
@@ -649,14 +651,15 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLane
     if (top) gA = gB;
   }
   float* o_g = LAST ? og + (size_t)r0 * W : nullptr;
+  int orow = r0;                                      // the row being output (the last step stores [slo, shi))
   // z row i from the window; x = raw row i + 2
   auto row = [&](const Vec4<N>& x, const Vec4<N>& ha, const Vec4<N>& hb, Vec4<N>& hc, const Vec4<N>& ga,
                  const Vec4<N>& gb, Vec4<N>& gc, bool bottom_row) {
     hc = seg_hraw<SEG>(x, L);
     gc = seg_hraw<SEG>(vert(ha, hb, hc, true), L);
     if (bottom_row) gc = gb;
-    seg_store<LAST>(L, ad, o_g, vert(ga, gb, gc, false));
-    if (LAST) o_g += W;
+    if (!LAST || (orow >= slo && orow < shi)) seg_store<LAST>(L, ad, o_g, vert(ga, gb, gc, false));
+    if (LAST) { o_g += W; ++orow; }
     ad += W4;
   };
   // rotation phases: P0 = (A, B, C), P1 = (B, C, A), P2 = (C, A, B)
@@ -701,13 +704,14 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLane
 
 template <int SEG, bool CLEAN, int N, bool LAST, bool E>
 __device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, const SegLanes<N, E>& L, float* og, int H,
-                                                 int W, int c, float2 aff, int r0, int Hp, int bar_id, int bar_threads) {
+                                                 int W, int c, float2 aff, int r0, int Hp, int bar_id, int bar_threads,
+                                                 int slo, int shi) {
   if (CLEAN) {
     switch (epi) {
-      case 0: inplace_step_clean<SEG, N, LAST, 0>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
-      case 1: inplace_step_clean<SEG, N, LAST, 1>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
-      case 2: inplace_step_clean<SEG, N, LAST, 2>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
-      default: inplace_step_clean<SEG, N, LAST, 3>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads); break;
+      case 0: inplace_step_clean<SEG, N, LAST, 0>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
+      case 1: inplace_step_clean<SEG, N, LAST, 1>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
+      case 2: inplace_step_clean<SEG, N, LAST, 2>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
+      default: inplace_step_clean<SEG, N, LAST, 3>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
     }
     return;
   }
@@ -778,12 +782,16 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
         const int s = k % a.stages;
         if (k >= a.stages) mbar_wait_sleep(&empty[s], ((k / a.stages) - 1) & 1);
-        const int64_t pl0 = t * a.tile_planes;
+        // whole planes: np contiguous planes; band tiles (n_bands > 1, one plane): rows [in_lo, in_hi)
+        const int64_t pg = t / a.n_bands;
+        const int band = (int)(t - pg * a.n_bands);
+        const SeqRange rg = a.ranges[(size_t)band * n];
+        const int64_t pl0 = pg * a.tile_planes;
         const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
-        const float* src = a.in + (a.plane0 + pl0) * (int64_t)HW;
+        const float* src = a.in + (a.plane0 + pl0) * (int64_t)HW + (a.n_bands > 1 ? (int64_t)rg.in_lo * W : 0);
         const uint32_t head_off = (uint32_t)((uintptr_t)src & 15u);
         float* dst = (float*)((char*)stage0 + (size_t)s * a.stage_bytes + head_off);
-        const uint32_t nbytes = (uint32_t)np * (uint32_t)HW * 4u;
+        const uint32_t nbytes = (uint32_t)np * (uint32_t)(a.n_bands > 1 ? (rg.in_hi - rg.in_lo) * W : HW) * 4u;
         const uint32_t h = min(nbytes, (16u - head_off) & 15u);
         const uint32_t body = (nbytes - h) & ~15u;
         for (uint32_t e = 0; e < h / 4; ++e) cp_async4(dst + e, src + e);
@@ -810,9 +818,6 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
   const int part = (cw % wpp) * (32 / SEG) + half;
   const int n_parts = wpp * (32 / SEG);
   const int Hp = (H + n_parts - 1) / n_parts;          // one-step kernel: equal parts (the last shorter)
-  // clean steps: balanced parts (equal whenever two parts share a warp, see inplace_mode)
-  const int c_r0 = CLEAN ? part * H / n_parts : part * Hp;
-  const int c_hp = CLEAN ? (part + 1) * H / n_parts - c_r0 : Hp;
   const int bar_id = wpp > 1 ? 1 + cw / wpp : 0;       // named barrier of the plane's warps
   float2* const t_aff = (float2*)(stage0 + (size_t)a.stages * a.stage_bytes) + (size_t)cw * n;   // this warp's
   // column segments: NSEG = 2 splits a row's W / 4 groups into two halves of GS groups
@@ -820,9 +825,26 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
   int k = 0;
   for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
     const int s = k % a.stages;
-    const int64_t pl0 = t * a.tile_planes;
+    const int64_t pg = t / a.n_bands;
+    const int band = (int)(t - pg * a.n_bands);
+    const int64_t pl0 = pg * a.tile_planes;
     const int np = (int)min((int64_t)a.tile_planes, a.n_planes - pl0);
     const int p = cw / wpp;                             // this warp's plane in the tile
+    // the tile's rows: a whole plane, or a band [in_lo, in_hi) of one plane (halo tiles, clean
+    // steps only): the band is swept like a plane whose edges are the band's; a non-plane band
+    // edge spoils one more row per step there, and only the last step's rows [out_lo, out_hi) --
+    // n steps inside such an edge -- are stored (the paper's patches)
+    int row0 = 0, Ht = H, st_lo = 0, st_hi = H;
+    if (a.n_bands > 1) {
+      const SeqRange r_in = a.ranges[(size_t)band * n], r_out = a.ranges[(size_t)band * n + n - 1];
+      row0 = r_in.in_lo;
+      Ht = r_in.in_hi - r_in.in_lo;
+      st_lo = r_out.out_lo - row0;
+      st_hi = r_out.out_hi - row0;
+    }
+    // clean steps: balanced parts (equal whenever two parts share a warp, see inplace_mode)
+    const int c_r0 = CLEAN ? part * Ht / n_parts : part * Hp;
+    const int c_hp = CLEAN ? (part + 1) * Ht / n_parts - c_r0 : Hp;
     const uint32_t plane = (uint32_t)(a.plane0 + pl0 + min(p, np - 1));
     // (scale, shift) of this warp's plane for every step, all loads in flight at once
     const uint32_t ch = plane - fdiv(plane, a.cdiv) * (uint32_t)a.C;
@@ -833,7 +855,7 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
     const char* sbase = (const char*)stage0 + (size_t)s * a.stage_bytes +
                         ((uintptr_t)(a.in + (a.plane0 + pl0) * (int64_t)HW) & 15u);
     const uint32_t base = smem_u32(sbase) + 4u * (uint32_t)(min(p, np - 1) * HW + c);
-    float* og = a.out + (int64_t)plane * HW + c;
+    float* og = a.out + (int64_t)plane * HW + (int64_t)row0 * W + c;
     // this lane's segments: pad lanes (outside the plane) read -inf and never store; halo lanes
     // (the neighbouring segment's edge group) read and never store
     SegLanes<NSEG, EDGE> L;
@@ -852,19 +874,21 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
       for (; st + 1 < n; st += 2) {
         const float lo1 = (epi_tab[st] & 1) ? 0.f : -CUDART_INF_F, lo2 = (epi_tab[st + 1] & 1) ? 0.f : -CUDART_INF_F;
         if (st + 2 == n)
-          inplace_pair_clean<SEG, NSEG, true>(base, L, og, H, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
-                                              bar_id, 32 * wpp);
+          inplace_pair_clean<SEG, NSEG, true>(base, L, og, Ht, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
+                                              bar_id, 32 * wpp, st_lo, st_hi);
         else
-          inplace_pair_clean<SEG, NSEG, false>(base, L, og, H, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
-                                               bar_id, 32 * wpp);
+          inplace_pair_clean<SEG, NSEG, false>(base, L, og, Ht, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
+                                               bar_id, 32 * wpp, st_lo, st_hi);
       }
     }
     for (; st < n; ++st) {
       const float2 aff = t_aff[st];
       if (st == n - 1)
-        inplace_step_epi<SEG, CLEAN, NSEG, true>(epi_tab[st], base, L, og, H, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp);
+        inplace_step_epi<SEG, CLEAN, NSEG, true>(epi_tab[st], base, L, og, Ht, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp,
+                                                 st_lo, st_hi);
       else
-        inplace_step_epi<SEG, CLEAN, NSEG, false>(epi_tab[st], base, L, og, H, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp);
+        inplace_step_epi<SEG, CLEAN, NSEG, false>(epi_tab[st], base, L, og, Ht, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp,
+                                                  st_lo, st_hi);
     }
     mbar_arrive(&empty[s]);   // every lane: the tile's stage is free for the producer
   }

@@ -59,6 +59,11 @@ FAMILIES = [
      "sequence_staged_tma"),
     ("seq_halo", synth.synthetic51(5, batch=2, C=C, H=64).layers, (2, C, 64, 64), {"force_rows_per_task": 7},
      "sequence_staged_tma"),
+    # halo (band) tiles swept in place: planes that do not fit whole under the budget
+    ("seq_inplace_bands", synth.synthetic51(7, batch=1, C=C, H=100).layers, (1, C, 100, 64),
+     {"smem_budget_bytes": 16384}, "sequence_staged_tma"),
+    ("seq_inplace_bands_2seg", synth.synthetic51(4, batch=1, C=2, H=80).layers, (1, 2, 80, 224),
+     {"smem_budget_bytes": 40960}, "sequence_staged_tma"),
     ("seq_generic", [synth.maxpool(3, 1, 1), synth.relu(), synth.avgpool(2, 2), synth.batchnorm(C, 8),
                      synth.maxpool(3, 2, 1)], (64, C, 24, 22), {"force_tile_planes": 1}, "sequence_staged_tma"),
 ]

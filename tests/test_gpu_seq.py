@@ -198,3 +198,32 @@ def test_random_fast_sequences(trial, cuda_dev, oracle_lib):
     U.assert_close(got, oracle.run_bf(layers, x), ctx)
     other, _ = run_gpu(layers, x, {"force_tile_planes": 1})
     U.assert_bitexact(got, other, ctx + " vs shared tile / halo")
+
+
+@pytest.mark.parametrize("H,W,budget,depth", [(224, 224, 110 * 1024, 16), (112, 112, 40 * 1024, 9),
+                                              (300, 200, 0, 12), (100, 64, 16 * 1024, 7), (61, 96, 12 * 1024, 6)])
+def test_inplace_band_tiles(H, W, budget, depth, cuda_dev, oracle_lib):
+    """Halo (band) tiles of §5.1 networks run in place (k_seq.cu seq_inplace band tiles): planes
+    that do not fit whole (wider than 224, or under a budget).  Every policy (planner, the paper's
+    unrestricted, <= 5 steps) against the oracle, and bit for bit against the shared-tile kernel's
+    halo tiles (force_tile_planes keeps seq_staged) and the unbudgeted whole-plane run."""
+    bs = _bs()
+    shape = (2, 3, H, W)
+    layers = []
+    for b in range(depth):
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(3, 60 + b, signed_gamma=b % 3 == 1)] + \
+                  ([synth.relu()] if b % 2 == 0 else [])
+    x = synth.uniform_np(H * 7 + W + depth, int(np.prod(shape))).reshape(shape)
+    ref = oracle.run_bf(layers, x[:1])
+    base = {"smem_budget_bytes": budget} if budget else {}
+    whole, _ = run_gpu(layers, x) if budget else (None, None)
+    for policy in (0, -1, 5):
+        got, plan = run_gpu(layers, x, {**base, "max_steps_per_sequence": policy})
+        li = bs.bs_plan_query_launch(plan, 0)
+        assert li["tile_rows"] > 0 and li["block"] in (160, 288) and li["smem_bytes"] < 2.2 * li["tile_rows"] * W * 4 + \
+            (2 * depth + 8) * W * 8 + 8192, li                         # band tiles, in place (no work buffer)
+        U.assert_close(got[:1], ref, f"H={H} W={W} policy {policy}")
+        staged, plan2 = run_gpu(layers, x, {**base, "max_steps_per_sequence": policy, "force_tile_planes": 1})
+        U.assert_bitexact(got, staged, f"H={H} W={W} policy {policy}: in place vs seq_staged bands")
+        if whole is not None:
+            U.assert_bitexact(got, whole, f"H={H} W={W} policy {policy}: bands vs whole planes")
