@@ -522,7 +522,7 @@ __device__ __forceinline__ void seg_store(const SegLanes<N, E>& L, uint32_t ad, 
     }
 }
 
-template <int SEG, int N, bool LAST, int EPI, bool E>
+template <int SEG, int N, bool LAST, int EPI, bool E, bool BAND>
 __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLanes<N, E>& L, float* og, int H, int W,
                                                    float2 aff, int r0, int Hp, int bar_id, int bar_threads, int slo,
                                                    int shi) {
@@ -552,7 +552,7 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
       o.s[q].z = epi(max3f(a.s[q].z, b.s[q].z, c.s[q].z));
       o.s[q].w = epi(max3f(a.s[q].w, b.s[q].w, c.s[q].w));
     }
-    if (!LAST || (orow >= slo && orow < shi)) seg_store<LAST>(L, ad, o_g, o);
+    if (!LAST || !BAND || (orow >= slo && orow < shi)) seg_store<LAST>(L, ad, o_g, o);
     if (LAST) { o_g += W; ++orow; }
     ad += W4;
   };
@@ -603,7 +603,7 @@ __device__ __forceinline__ void inplace_step_clean(uint32_t pbase, const SegLane
 // BN (exact: v + -0 == v, -0 included) and lo = -inf without ReLU.  The window rotates through
 // three register roles (no moves): the main loop is unrolled by 3 and the part's last 2..5 rows
 // are unrolled per remainder.
-template <int SEG, int N, bool LAST, bool E>
+template <int SEG, int N, bool LAST, bool E, bool BAND>
 __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLanes<N, E>& L, float* og, int H, int W,
                                                    float2 a1, float lo1, float2 a2, float lo2, int r0, int Hp,
                                                    int bar_id, int bar_threads, int slo, int shi) {
@@ -658,7 +658,7 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLane
     hc = seg_hraw<SEG>(x, L);
     gc = seg_hraw<SEG>(vert(ha, hb, hc, true), L);
     if (bottom_row) gc = gb;
-    if (!LAST || (orow >= slo && orow < shi)) seg_store<LAST>(L, ad, o_g, vert(ga, gb, gc, false));
+    if (!LAST || !BAND || (orow >= slo && orow < shi)) seg_store<LAST>(L, ad, o_g, vert(ga, gb, gc, false));
     if (LAST) { o_g += W; ++orow; }
     ad += W4;
   };
@@ -702,16 +702,16 @@ __device__ __forceinline__ void inplace_pair_clean(uint32_t pbase, const SegLane
   else __syncwarp();
 }
 
-template <int SEG, bool CLEAN, int N, bool LAST, bool E>
+template <int SEG, bool CLEAN, int N, bool LAST, bool E, bool BAND>
 __device__ __forceinline__ void inplace_step_epi(int epi, uint32_t base, const SegLanes<N, E>& L, float* og, int H,
                                                  int W, int c, float2 aff, int r0, int Hp, int bar_id, int bar_threads,
                                                  int slo, int shi) {
   if (CLEAN) {
     switch (epi) {
-      case 0: inplace_step_clean<SEG, N, LAST, 0>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
-      case 1: inplace_step_clean<SEG, N, LAST, 1>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
-      case 2: inplace_step_clean<SEG, N, LAST, 2>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
-      default: inplace_step_clean<SEG, N, LAST, 3>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
+      case 0: inplace_step_clean<SEG, N, LAST, 0, E, BAND>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
+      case 1: inplace_step_clean<SEG, N, LAST, 1, E, BAND>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
+      case 2: inplace_step_clean<SEG, N, LAST, 2, E, BAND>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
+      default: inplace_step_clean<SEG, N, LAST, 3, E, BAND>(base, L, og, H, W, aff, r0, Hp, bar_id, bar_threads, slo, shi); break;
     }
     return;
   }
@@ -742,7 +742,7 @@ __host__ __device__ inline int inplace_mode(int seg, int tile_planes, int H, int
   return W / 4 + 2 <= seg ? 1 : 2;
 }
 
-template <int SEG, int MODE, int NSEG>
+template <int SEG, int MODE, int NSEG, bool BAND>
 __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ? 1 : 4) seq_inplace(SeqArgs a) {
   constexpr int WARPS = inplace_warps_of(NSEG);
   constexpr bool CLEAN = MODE != 0, EDGE = MODE == 2;
@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
     // edge spoils one more row per step there, and only the last step's rows [out_lo, out_hi) --
     // n steps inside such an edge -- are stored (the paper's patches)
     int row0 = 0, Ht = H, st_lo = 0, st_hi = H;
-    if (a.n_bands > 1) {
+    if (BAND) {
       const SeqRange r_in = a.ranges[(size_t)band * n], r_out = a.ranges[(size_t)band * n + n - 1];
       row0 = r_in.in_lo;
       Ht = r_in.in_hi - r_in.in_lo;
@@ -874,20 +874,20 @@ __global__ void __launch_bounds__(32 * (inplace_warps_of(NSEG) + 1), NSEG == 2 ?
       for (; st + 1 < n; st += 2) {
         const float lo1 = (epi_tab[st] & 1) ? 0.f : -CUDART_INF_F, lo2 = (epi_tab[st + 1] & 1) ? 0.f : -CUDART_INF_F;
         if (st + 2 == n)
-          inplace_pair_clean<SEG, NSEG, true>(base, L, og, Ht, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
+          inplace_pair_clean<SEG, NSEG, true, EDGE, BAND>(base, L, og, Ht, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
                                               bar_id, 32 * wpp, st_lo, st_hi);
         else
-          inplace_pair_clean<SEG, NSEG, false>(base, L, og, Ht, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
+          inplace_pair_clean<SEG, NSEG, false, EDGE, BAND>(base, L, og, Ht, W, t_aff[st], lo1, t_aff[st + 1], lo2, c_r0, c_hp,
                                                bar_id, 32 * wpp, st_lo, st_hi);
       }
     }
     for (; st < n; ++st) {
       const float2 aff = t_aff[st];
       if (st == n - 1)
-        inplace_step_epi<SEG, CLEAN, NSEG, true>(epi_tab[st], base, L, og, Ht, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp,
+        inplace_step_epi<SEG, CLEAN, NSEG, true, EDGE, BAND>(epi_tab[st], base, L, og, Ht, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp,
                                                  st_lo, st_hi);
       else
-        inplace_step_epi<SEG, CLEAN, NSEG, false>(epi_tab[st], base, L, og, Ht, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp,
+        inplace_step_epi<SEG, CLEAN, NSEG, false, EDGE, BAND>(epi_tab[st], base, L, og, Ht, W, c, aff, c_r0, c_hp, bar_id, 32 * wpp,
                                                   st_lo, st_hi);
     }
     mbar_arrive(&empty[s]);   // every lane: the tile's stage is free for the producer
@@ -901,14 +901,18 @@ size_t seq_inplace_smem(const SeqArgs& a) {
 }
 
 static const void* seq_fn(const SeqArgs& a) {
-  if (a.inplace_seg && inplace_nseg(a.W0) == 2) return (const void*)seq_inplace<32, 1, 2>;
+  const bool band = a.n_bands > 1;   // in-place band tiles: 32-lane segments, clean steps only
+  if (a.inplace_seg && inplace_nseg(a.W0) == 2)
+    return band ? (const void*)seq_inplace<32, 1, 2, true> : (const void*)seq_inplace<32, 1, 2, false>;
   const int mode = a.inplace_seg ? inplace_mode(a.inplace_seg, a.tile_planes, a.H0, a.W0) : 0;
+  if (a.inplace_seg == 32 && band)
+    return mode == 2 ? (const void*)seq_inplace<32, 2, 1, true> : (const void*)seq_inplace<32, 1, 1, true>;
   if (a.inplace_seg == 16)
-    return mode == 1 ? (const void*)seq_inplace<16, 1, 1> : mode == 2 ? (const void*)seq_inplace<16, 2, 1>
-                                                                        : (const void*)seq_inplace<16, 0, 1>;
+    return mode == 1 ? (const void*)seq_inplace<16, 1, 1, false> : mode == 2 ? (const void*)seq_inplace<16, 2, 1, false>
+                                                                               : (const void*)seq_inplace<16, 0, 1, false>;
   if (a.inplace_seg == 32)
-    return mode == 1 ? (const void*)seq_inplace<32, 1, 1> : mode == 2 ? (const void*)seq_inplace<32, 2, 1>
-                                                                        : (const void*)seq_inplace<32, 0, 1>;
+    return mode == 1 ? (const void*)seq_inplace<32, 1, 1, false> : mode == 2 ? (const void*)seq_inplace<32, 2, 1, false>
+                                                                               : (const void*)seq_inplace<32, 0, 1, false>;
   return (const void*)seq_staged;
 }
 
