@@ -170,7 +170,7 @@ def test_inplace_wide_planes(H, W, cuda_dev, oracle_lib):
         U.assert_bitexact(got, other, f"H={H} W={W} in-place vs shared tile / halo")
 
 
-@pytest.mark.parametrize("trial", range(48))
+@pytest.mark.parametrize("trial", range(64))
 def test_random_fast_sequences(trial, cuda_dev, oracle_lib):
     """Random sequences of §5.1-type steps (3x3/s1/p1 max + any of BN (signed gamma) / ReLU / none)
     on random planes (W a multiple of 4 up to 224, H 1..70 or up to 224): every sequence kernel the
@@ -192,11 +192,13 @@ def test_random_fast_sequences(trial, cuda_dev, oracle_lib):
         if rng.random() < 0.6:
             layers.append(synth.relu())
     shape = (N, C, H, W)
+    # a third of the trials under a small shared-memory budget: halo (band) tiles, in place or shared
+    opts = {"smem_budget_bytes": rng.choice([8, 12, 16, 24, 32, 48]) * 1024} if rng.random() < 0.35 else {}
     x = synth.uniform_np(7000 + trial, int(np.prod(shape))).reshape(shape)
-    got, plan = run_gpu(layers, x)
-    ctx = f"trial {trial} shape {shape} {len(layers)} layers {_bs().bs_plan_query_launch(plan, 0)}"
+    got, plan = run_gpu(layers, x, opts or None)
+    ctx = f"trial {trial} shape {shape} {len(layers)} layers {opts} {_bs().bs_plan_query_launch(plan, 0)}"
     U.assert_close(got, oracle.run_bf(layers, x), ctx)
-    other, _ = run_gpu(layers, x, {"force_tile_planes": 1})
+    other, _ = run_gpu(layers, x, {**opts, "force_tile_planes": 1})
     U.assert_bitexact(got, other, ctx + " vs shared tile / halo")
 
 
