@@ -113,6 +113,30 @@ def test_large_planes_use_halo_tiles(bs):
     assert bs.bs_plan_query(p)["n_sequences"] == 1 and li["tile_rows"] == 0 and li["halo_rows"] == 0
 
 
+def test_band_tiles_run_in_place(bs):
+    """Halo (band) sequences of §5.1-type steps on planes 57..224 wide run in the in-place kernel
+    (its two stages hold only the band: no work buffer) with balanced bands; planes wider than 224
+    keep the shared-tile kernel (stage + work buffer)."""
+    layers = []
+    for b in range(6):
+        layers += [synth.maxpool(3, 1, 1), synth.batchnorm(2, b), synth.relu()]
+    for shape, budget, in_place in (((1, 2, 224, 224), 110 * 1024, True), ((1, 2, 112, 112), 40 * 1024, True),
+                                    ((1, 2, 100, 64), 16 * 1024, True), ((1, 2, 240, 240), 0, False)):
+        p = host_plan(bs, layers, shape, **({"smem_budget_bytes": budget} if budget else {}))
+        li = bs.bs_plan_query_launch(p, 0)
+        W = shape[3]
+        band_in = li["tile_rows"] + 2 * li["groups_per_warp"]      # output rows + one halo row per step and side
+        assert li["tile_rows"] > 0, li
+        if in_place:
+            assert li["block"] == (288 if W > 128 else 160), li
+            assert li["smem_bytes"] <= 2 * (band_in * W * 4 + 16 + 127) + 128 + 6 * 8 * 8 + 1024 + 256, li
+            assert li["smem_bytes"] <= (budget or 220 * 1024)
+            # balanced bands: every band within one row of the others
+            assert -(-shape[2] // li["tile_rows"]) * li["tile_rows"] - shape[2] < -(-shape[2] // li["tile_rows"]), li
+        else:
+            assert li["block"] == 288 and li["smem_bytes"] > 2 * band_in * W * 4, li   # stages + work buffer
+
+
 def _sec51_split_depth(W, H, budget=110 * 1024, lanes=256):
     """Independent closed form of the paper's packing rule for §5.1 blocks on H x W
     planes with halo tiles: base tile = ceil(256 / W) output rows (one output per consumer lane),
