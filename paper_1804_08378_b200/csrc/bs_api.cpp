@@ -609,7 +609,7 @@ int64_t inplace_smem(const std::vector<Step>& steps, size_t a, size_t b, const b
   for (size_t k = a; k < b; ++k)
     if (!is_fast_step(steps[k]) || steps[k].in.w != W || steps[k].in.h != H) return -1;
   // planes 129..224 wide: one plane per CTA, 8 warps each owning ~H / 8 rows of both column
-  // segments of the row (k_seq.cu seq_inplace<32, 1, 2>); parts of >= 2 rows
+  // segments of the row (k_seq.cu seq_inplace<32, 1, 2, false>); parts of >= 2 rows
   const bool wide = W > 128;
   if (wide && H < 16) return -1;
   const int64_t warps = wide ? 8 : kInplaceWarps;

@@ -149,7 +149,7 @@ def test_inplace_kernel_heights(H, cuda_dev, oracle_lib):
 
 @pytest.mark.parametrize("H,W", [(16, 132), (24, 200), (40, 160), (56, 224), (224, 224), (30, 144), (51, 224)])
 def test_inplace_wide_planes(H, W, cuda_dev, oracle_lib):
-    """Planes 129..224 wide run in place too (k_seq.cu seq_inplace<32, 1, 2>): one plane per CTA,
+    """Planes 129..224 wide run in place too (k_seq.cu seq_inplace<32, 1, 2, false>): one plane per CTA,
     8 warps of ~H / 8 rows (balanced, unequal when 8 does not divide H), each row as two column
     segments with halo lanes; even and odd step
     counts (two-step sweeps + a single step), signed-gamma BN; bit for bit equal to the
